@@ -1,0 +1,232 @@
+// Memory-bound kernels of the hybrid step:
+// embedding gather, RMSNorm (fp32 residual stream -> bf16), RoPE + paged KV
+// append, greedy argmax sampling, deterministic weight init and the KV page
+// migration copy. All use 16 B vector accesses and warp-shuffle reductions.
+#pragma once
+
+#include "common.cuh"
+
+namespace tc {
+
+// ---------------------------------------------------------------- weight init
+// value = ((u24 * 2^-24) * 2 - 1) * scale + offset, u24 = top 24 bits of
+// splitmix64(splitmix64(seed ^ splitmix64(tensor_id)) + logical_index), computed
+// with explicitly rounded fp32 ops so the numpy oracle reproduces every bit.
+__host__ __device__ inline uint64_t sm64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// interleave64 != 0: physical row p of a [2*F, K] gate|up matrix stores logical
+// row (p/128)*64 + p%64 of gate (p%128 < 64) or of up (tensor_id + 1).
+__global__ void init_weights(__nv_bfloat16* dst, long long rows, long long cols, uint64_t seed, uint64_t tensor_id,
+                             float scale, float offset, int interleave64) {
+  const long long n = rows * cols;
+  const uint64_t key_a = sm64(seed ^ sm64(tensor_id));
+  const uint64_t key_b = sm64(seed ^ sm64(tensor_id + 1));
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long prow = i / cols, col = i % cols;
+    long long lrow = prow;
+    uint64_t key = key_a;
+    if (interleave64) {
+      const long long blk = prow / 128, within = prow % 128;
+      lrow = blk * 64 + (within % 64);
+      key = within < 64 ? key_a : key_b;
+    }
+    const uint64_t h = sm64(key + (uint64_t)(lrow * cols + col));
+    const float u = (float)(uint32_t)(h >> 40) * 5.9604644775390625e-08f;  // exact
+    const float c = u * 2.0f - 1.0f;                                          // exact
+    const float v = __fadd_rn(__fmul_rn(c, scale), offset);
+    dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// ---------------------------------------------------------------- embedding
+// resid[t, :] = float(embed[tokens[t], :])
+__global__ void embed_rows(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed,
+                           float* __restrict__ resid, int d) {
+  const int t = blockIdx.x;
+  const __nv_bfloat16* src = embed + (long long)tokens[t] * d;
+  float* dst = resid + (long long)t * d;
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src + c);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = unpack_bf16(w[e]);
+      dst[c + 2 * e] = f.x;
+      dst[c + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// out[r, :] = bf16(x[src_row(r), :] * rsqrt(mean(x^2) + eps) * w), fp32 math.
+// rows == nullptr: identity row map; otherwise gathers rows (sampled-row LM head).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict__ x, const int* __restrict__ rows,
+                                                        const __nv_bfloat16* __restrict__ w,
+                                                        __nv_bfloat16* __restrict__ out, int d, float eps) {
+  const int r = blockIdx.x;
+  const int src = rows ? rows[r] : r;
+  const float* xr = x + (long long)src * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[THREADS / 32];
+  ss = warp_sum(ss);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)d + eps);
+  __nv_bfloat16* o = out + (long long)r * d;
+  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    const uint2 wb = *reinterpret_cast<const uint2*>(w + c);
+    const float2 w01 = unpack_bf16(wb.x), w23 = unpack_bf16(wb.y);
+    uint2 pk;
+    pk.x = pack_bf16(v.x * inv * w01.x, v.y * inv * w01.y);
+    pk.y = pack_bf16(v.z * inv * w23.x, v.w * inv * w23.y);
+    *reinterpret_cast<uint2*>(o + c) = pk;
+  }
+}
+
+// ---------------------------------------------------------------- RoPE + KV append
+// For packed row t: rotate q heads in place (half-split / rotate_half convention)
+// and write rotated k and raw v into the paged pool at (block_table[pos/PS], pos%PS).
+// rope_cs: [max_pos][DH/2] float2 (cos, sin), computed on the host in fp64.
+struct RopeAppendParams {
+  __nv_bfloat16* qkv;
+  __nv_bfloat16* kv;
+  const float2* rope_cs;
+  const int* positions;
+  const int* row_seq;
+  const int* seq_bt_off;
+  const int* block_tables;
+  long long page_stride;
+  int layer, n_heads, n_kv_heads, head_dim, page_size;
+};
+
+__global__ void rope_kv_append(RopeAppendParams p) {
+  const int t = blockIdx.x;
+  const int pos = p.positions[t];
+  const int seq = p.row_seq[t];
+  const int page = p.block_tables[p.seq_bt_off[seq] + pos / p.page_size];
+  const int slot = pos % p.page_size;
+  const int half = p.head_dim / 2;
+  const int ld = (p.n_heads + 2 * p.n_kv_heads) * p.head_dim;
+  __nv_bfloat16* row = p.qkv + (long long)t * ld;
+  const float2* cs = p.rope_cs + (long long)pos * half;
+  __nv_bfloat16* page_base = p.kv + (long long)page * p.page_stride;
+  const int n_rot = (p.n_heads + p.n_kv_heads) * half;
+  for (int i = threadIdx.x; i < n_rot; i += blockDim.x) {
+    const int h = i / half, j = i % half;
+    __nv_bfloat16* x = row + h * p.head_dim;
+    const float x1 = __bfloat162float(x[j]), x2 = __bfloat162float(x[j + half]);
+    const float2 c = cs[j];
+    const float y1 = x1 * c.x - x2 * c.y;
+    const float y2 = x2 * c.x + x1 * c.y;
+    if (h < p.n_heads) {
+      x[j] = __float2bfloat16(y1);
+      x[j + half] = __float2bfloat16(y2);
+    } else {
+      const int kvh = h - p.n_heads;
+      __nv_bfloat16* dst = page_base + (((long long)(p.layer * 2) * p.n_kv_heads + kvh) * p.page_size + slot) * p.head_dim;
+      dst[j] = __float2bfloat16(y1);
+      dst[j + half] = __float2bfloat16(y2);
+    }
+  }
+  const int n_v = p.n_kv_heads * p.head_dim / 8;
+  for (int i = threadIdx.x; i < n_v; i += blockDim.x) {
+    const int kvh = (i * 8) / p.head_dim, c = (i * 8) % p.head_dim;
+    const uint4 v = *reinterpret_cast<const uint4*>(row + (p.n_heads + p.n_kv_heads + kvh) * p.head_dim + c);
+    __nv_bfloat16* dst =
+        page_base + (((long long)(p.layer * 2 + 1) * p.n_kv_heads + kvh) * p.page_size + slot) * p.head_dim + c;
+    *reinterpret_cast<uint4*>(dst) = v;
+  }
+}
+
+// ---------------------------------------------------------------- greedy sampling
+// ids[r] = argmax_v logits[r, v], lowest index on ties.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) argmax_rows(const float* __restrict__ logits, int vocab, int* __restrict__ ids) {
+  const float* row = logits + (long long)blockIdx.x * vocab;
+  float best = -INFINITY;
+  int best_i = 0x7fffffff;
+  for (int c = threadIdx.x * 4; c < vocab; c += THREADS * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(row + c);
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (e[k] > best) {  // strictly greater keeps the lowest index within a thread
+        best = e[k];
+        best_i = c + k;
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (ob > best || (ob == best && oi < best_i)) {
+      best = ob;
+      best_i = oi;
+    }
+  }
+  __shared__ float sb[THREADS / 32];
+  __shared__ int si[THREADS / 32];
+  if (threadIdx.x % 32 == 0) {
+    sb[threadIdx.x / 32] = best;
+    si[threadIdx.x / 32] = best_i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < THREADS / 32; ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < best_i)) {
+        best = sb[w];
+        best_i = si[w];
+      }
+    ids[blockIdx.x] = best_i;
+  }
+}
+
+// ---------------------------------------------------------------- KV migration
+// Copies whole pages (all layers) of one request: dst_pool[dst_pages[i]] = src_pool[src_pages[i]].
+// Pools may live on different GPUs (peer pointers over NVLink, UVA); one
+// launch moves every page of the request with 16 B loads, several in flight per thread.
+__global__ void __launch_bounds__(512) kv_copy_pages(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
+                                                     const int* __restrict__ src_pages, const int* __restrict__ dst_pages,
+                                                     int n_pages, long long page_vec) {
+  const long long total = (long long)n_pages * page_vec;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total; base += stride * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < total) {
+        const long long pg = i / page_vec, off = i % page_vec;
+        v[u] = ld_nc_v4(src_pool + (long long)src_pages[pg] * page_vec + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < total) {
+        const long long pg = i / page_vec, off = i % page_vec;
+        st_global_v4(dst_pool + (long long)dst_pages[pg] * page_vec + off, v[u]);
+      }
+    }
+  }
+}
+
+}  // namespace tc

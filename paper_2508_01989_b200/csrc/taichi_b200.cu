@@ -1,0 +1,1120 @@
+// libtaichi_b200 -- implementation of include/taichi_b200.h.
+//
+// One tc_instance = one TaiChi instance = one GPU stream holding a full model
+// replica (no tensor parallelism: Llama-3-8B / Qwen2.5-14B fit one B200), a
+// page-major paged KV pool and the step workspaces. A hybrid step (the GPU
+// form of BatchPlan) is packed as [prefill slice rows | decode rows] and runs:
+//   embed -> L x [RMSNorm -> QKV GEMM (+bias) -> RoPE + paged KV append ->
+//   chunked-prefill attention | split-KV decode attention -> O GEMM (+resid) ->
+//   RMSNorm -> gate_up GEMM (+SwiGLU) -> down GEMM (+resid)] ->
+//   RMSNorm on sampled rows only -> LM-head GEMM -> argmax.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "gemm.cuh"
+#include "taichi_b200.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct TcFail {
+  tc_status code;
+  std::string msg;
+};
+
+#define TC_CUDA(x)                                                                                     \
+  do {                                                                                                 \
+    cudaError_t e_ = (x);                                                                              \
+    if (e_ != cudaSuccess)                                                                             \
+      throw TcFail{TC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + std::to_string(__LINE__)}; \
+  } while (0)
+#define TC_REQUIRE(cond, msg)                       \
+  do {                                              \
+    if (!(cond)) throw TcFail{TC_ERR_INVALID, msg}; \
+  } while (0)
+
+template <typename F>
+tc_status guarded(F&& f) {
+  try {
+    f();
+    return TC_OK;
+  } catch (const TcFail& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TC_ERR_INVALID;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------------ TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw TcFail{TC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable"};
+  return fn;
+}
+
+// Row-major bf16 [rows, cols] matrix, box = 64 (K) x box_rows, 128 B swizzle.
+CUtensorMap make_kmajor_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TcFail{TC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+  return m;
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+int device_sms(int dev) {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  TC_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  cache[dev] = n;
+  return n;
+}
+
+template <int BN, int EPI>
+void set_gemm_smem() {
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               tc::GemmCfg<BN>::kSmemBytes));
+}
+
+void init_kernel_attrs(int dev) {
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return;
+  DeviceGuard g(dev);
+  set_gemm_smem<64, 0>(); set_gemm_smem<64, 1>(); set_gemm_smem<64, 2>(); set_gemm_smem<64, 4>(); set_gemm_smem<64, 5>();
+  set_gemm_smem<128, 0>(); set_gemm_smem<128, 1>(); set_gemm_smem<128, 2>(); set_gemm_smem<128, 3>(); set_gemm_smem<128, 4>(); set_gemm_smem<128, 5>();
+  set_gemm_smem<256, 0>(); set_gemm_smem<256, 1>(); set_gemm_smem<256, 2>(); set_gemm_smem<256, 3>(); set_gemm_smem<256, 4>(); set_gemm_smem<256, 5>();
+  auto attr = [](const void* fn, int bytes) {
+    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  };
+  attr((const void*)tc::attn_prefill<64, 2>, 2 * tc::AttnTile<64>::kStageElems * 2);
+  attr((const void*)tc::attn_prefill<128, 4>, 2 * tc::AttnTile<128>::kStageElems * 2);
+  attr((const void*)tc::attn_prefill<128, 5>, 2 * tc::AttnTile<128>::kStageElems * 2);
+  attr((const void*)tc::attn_decode<64, 2>, 3 * tc::AttnTile<64>::kStageElems * 2);
+  attr((const void*)tc::attn_decode<128, 4>, 3 * tc::AttnTile<128>::kStageElems * 2);
+  attr((const void*)tc::attn_decode<128, 5>, 3 * tc::AttnTile<128>::kStageElems * 2);
+  done.insert(dev);
+}
+
+struct GemmChoice {
+  int bn, k_splits, m_tiles, n_tiles, kbps;
+};
+
+int largest_divisor_leq(int n, int cap) {
+  for (int d = std::max(1, std::min(cap, n)); d >= 1; --d)
+    if (n % d == 0) return d;
+  return 1;
+}
+
+GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits, size_t ws_floats) {
+  GemmChoice c{};
+  c.m_tiles = (M + tc::kGemmBM - 1) / tc::kGemmBM;
+  const int kb = K / tc::kGemmBK;
+  if (force_bn) {
+    c.bn = force_bn;
+  } else {
+    c.bn = (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : 64);
+    // fewer than ~3/4 of the SMs busy: narrower tiles
+    while (c.bn > 128 && c.m_tiles * (N / c.bn) < (sms * 3) / 4 && N % (c.bn / 2) == 0) c.bn /= 2;
+    if (epi != tc::EPI_SWIGLU && c.bn == 128 && c.m_tiles * (N / 128) < sms / 2 && N % 64 == 0) c.bn = 64;
+  }
+  c.n_tiles = N / c.bn;
+  const int units = c.m_tiles * c.n_tiles;
+  int splits = 1;
+  if (force_splits > 0) {
+    splits = force_splits;
+  } else if (force_splits == 0 && units < sms && M <= 256) {
+    // weight-streaming regime: split K so every SM pulls weights
+    const int want = (sms + units - 1) / units;
+    splits = largest_divisor_leq(kb, std::min(want, std::max(1, kb / 4)));
+  }
+  while (splits > 1 && (size_t)splits * M * N > ws_floats) splits = largest_divisor_leq(kb, splits - 1);
+  c.k_splits = splits;
+  c.kbps = kb / splits;
+  return c;
+}
+
+template <int BN>
+void launch_gemm_bn(const CUtensorMap& ma, const CUtensorMap& mb, const tc::GemmArgs& args, int epi, int grid,
+                    cudaStream_t s) {
+  const int smem = tc::GemmCfg<BN>::kSmemBytes;
+  switch (epi) {
+    case tc::EPI_BF16: tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_BF16_BIAS: tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_RESID_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_PARTIAL_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_PARTIAL_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_SWIGLU:
+      if constexpr (BN >= 128) {
+        tc::gemm_bf16_tcgen05<BN, tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args);
+        break;
+      }
+      [[fallthrough]];
+    default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue/tile"};
+  }
+}
+
+// Weight matrix with TMA maps for each tile width.
+struct WMat {
+  __nv_bfloat16* ptr = nullptr;
+  int64_t rows = 0, cols = 0;
+  CUtensorMap map64, map128, map256;
+  void make_maps() {
+    map64 = make_kmajor_map(ptr, rows, cols, 64);
+    if (rows % 128 == 0) map128 = make_kmajor_map(ptr, rows, cols, 128);
+    if (rows % 256 == 0) map256 = make_kmajor_map(ptr, rows, cols, 256);
+  }
+  const CUtensorMap& map(int bn) const { return bn == 64 ? map64 : (bn == 128 ? map128 : map256); }
+};
+
+// out = epi(A[M,K] * W[N,K]^T). a_map: box 128 rows over the activation buffer.
+int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
+             int sms, float* ws, size_t ws_floats, cudaStream_t s, int force_bn = 0, int force_splits = 0) {
+  const int N = (int)w.rows, K = (int)w.cols;
+  TC_REQUIRE(K % tc::kGemmBK == 0, "gemm: K must be a multiple of 64");
+  GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits, ws ? ws_floats : 0);
+  TC_REQUIRE(N % c.bn == 0, "gemm: N not divisible by tile width");
+  tc::GemmArgs args{};
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.m_tiles = c.m_tiles;
+  args.n_tiles = c.n_tiles;
+  args.k_splits = c.k_splits;
+  args.k_blocks_per_split = c.kbps;
+  args.bias = bias;
+  const int units = c.m_tiles * c.n_tiles * c.k_splits;
+  const int grid = std::min(units, sms);
+  if (c.k_splits == 1) {
+    args.out = out;
+    args.ldo = ldo;
+    switch (c.bn) {
+      case 64: launch_gemm_bn<64>(a_map, w.map(64), args, epi, grid, s); break;
+      case 128: launch_gemm_bn<128>(a_map, w.map(128), args, epi, grid, s); break;
+      default: launch_gemm_bn<256>(a_map, w.map(256), args, epi, grid, s); break;
+    }
+  } else {
+    args.out = ws;
+    args.ldo = N;
+    switch (c.bn) {
+      case 64: launch_gemm_bn<64>(a_map, w.map(64), args, tc::EPI_PARTIAL_F32, grid, s); break;
+      case 128: launch_gemm_bn<128>(a_map, w.map(128), args, tc::EPI_PARTIAL_F32, grid, s); break;
+      default: launch_gemm_bn<256>(a_map, w.map(256), args, tc::EPI_PARTIAL_F32, grid, s); break;
+    }
+    const int blocks = std::min(4 * sms, (int)(((size_t)M * N / 4 + 255) / 256) + 1);
+    switch (epi) {
+      case tc::EPI_BF16: tc::gemm_splitk_reduce<tc::EPI_BF16><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
+      case tc::EPI_BF16_BIAS: tc::gemm_splitk_reduce<tc::EPI_BF16_BIAS><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
+      case tc::EPI_RESID_F32: tc::gemm_splitk_reduce<tc::EPI_RESID_F32><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
+      case tc::EPI_SWIGLU: tc::gemm_splitk_reduce<tc::EPI_SWIGLU><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
+      case tc::EPI_F32: tc::gemm_splitk_reduce<tc::EPI_F32><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
+      default: throw TcFail{TC_ERR_INVALID, "bad epilogue"};
+    }
+  }
+  TC_CUDA(cudaGetLastError());
+  return c.k_splits == 1 ? 1 : 2;
+}
+
+// ------------------------------------------------------------------ instance
+struct LayerW {
+  WMat qkv, o, gate_up, down;
+  __nv_bfloat16 *qkv_bias = nullptr, *attn_norm = nullptr, *mlp_norm = nullptr;
+};
+
+constexpr uint64_t kTidEmbed = 1, kTidLmHead = 2, kTidFinalNorm = 3;
+inline uint64_t tid_layer(int l, int j) { return 16 + 16ull * l + j; }
+constexpr float kLinScale = 0.034641016f;  // uniform(-a, a) with std 0.02
+constexpr float kBiasScale = 0.1f;
+constexpr float kNormScale = 0.1f;
+
+struct PhaseTimer {
+  bool on = false;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      TC_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void reset() {
+    marks.clear();
+    used = 0;
+  }
+};
+
+}  // namespace
+
+struct tc_instance {
+  tc_instance_desc desc{};
+  tc_model_dims d{};
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  // weights
+  void* weight_block = nullptr;
+  __nv_bfloat16 *embed = nullptr, *final_norm = nullptr;
+  WMat lm_head;
+  std::vector<LayerW> layers;
+  // KV pool
+  __nv_bfloat16* kv = nullptr;
+  int64_t page_elems = 0, n_pages = 0;
+  std::vector<int32_t> free_pages;
+  std::unordered_map<int64_t, std::vector<int32_t>> tables;
+  // activations
+  int qkv_n = 0;
+  float* resid = nullptr;
+  __nv_bfloat16 *xnorm = nullptr, *qkv = nullptr, *attn_out = nullptr, *act = nullptr, *lm_in = nullptr;
+  float* logits = nullptr;
+  int* ids_dev = nullptr;
+  int* ids_host = nullptr;
+  CUtensorMap map_xnorm, map_attn, map_act, map_lm_in;
+  float* splitk_ws = nullptr;
+  size_t splitk_floats = 0;
+  float *attn_ws_o = nullptr, *attn_ws_ml = nullptr;
+  size_t attn_ws_floats = 0;
+  float2* rope = nullptr;
+  // per-step metadata
+  int32_t* meta_host = nullptr;
+  int32_t* meta_dev = nullptr;
+  size_t meta_ints = 0;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  bool step_pending = false;
+  int last_sampled = 0;
+  int launches = 0;       // kernels launched by the last step
+  int64_t h2d_bytes = 0;  // bytes copied H2D by the last step
+
+  // migration
+  int32_t* mig_host = nullptr;
+  int32_t* mig_dev = nullptr;
+  int mig_cap = 0;
+  cudaEvent_t mig_a = nullptr, mig_b = nullptr;
+  bool mig_pending = false;
+  int64_t mig_bytes = 0;
+  PhaseTimer prof;
+};
+
+namespace {
+
+tc_model_dims preset(const std::string& full) {
+  std::string name = full;
+  int layers_override = -1;
+  auto colon = full.find(":L");
+  if (colon != std::string::npos) {
+    name = full.substr(0, colon);
+    layers_override = std::stoi(full.substr(colon + 2));
+  }
+  tc_model_dims m{};
+  if (name == "tiny") {
+    m = {2, 256, 4, 2, 64, 512, 1024, 0, 1.0e4f, 1e-5f};
+  } else if (name == "llama3_8b") {
+    m = {32, 4096, 32, 8, 128, 14336, 128256, 0, 5.0e5f, 1e-5f};
+  } else if (name == "qwen2_5_14b") {
+    m = {48, 5120, 40, 8, 128, 13824, 152064, 1, 1.0e6f, 1e-6f};
+  } else {
+    throw TcFail{TC_ERR_INVALID, "unknown model preset " + name};
+  }
+  if (layers_override > 0) m.n_layers = layers_override;
+  return m;
+}
+
+void check_dims(const tc_model_dims& m) {
+  TC_REQUIRE(m.n_layers >= 1 && m.d_model >= 64, "dims: bad sizes");
+  TC_REQUIRE(m.head_dim == 64 || m.head_dim == 128, "dims: head_dim must be 64 or 128");
+  TC_REQUIRE(m.n_heads % m.n_kv_heads == 0, "dims: n_heads % n_kv_heads");
+  const int g = m.n_heads / m.n_kv_heads;
+  TC_REQUIRE((m.head_dim == 64 && g == 2) || (m.head_dim == 128 && (g == 4 || g == 5)),
+             "dims: supported (head_dim, group) = (64,2), (128,4), (128,5)");
+  TC_REQUIRE(m.d_model % 128 == 0 && m.ffn_dim % 64 == 0 && m.vocab % 128 == 0, "dims: alignment");
+}
+
+void init_tensor(__nv_bfloat16* p, int64_t rows, int64_t cols, uint64_t seed, uint64_t tid, float scale, float offset,
+                 int interleave, cudaStream_t s) {
+  const int64_t n = rows * cols;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 65536);
+  tc::init_weights<<<blocks, 256, 0, s>>>(p, rows, cols, seed, tid, scale, offset, interleave);
+  TC_CUDA(cudaGetLastError());
+}
+
+void* carve(uint8_t*& cur, size_t bytes) {
+  void* p = cur;
+  cur += (bytes + 255) & ~size_t(255);
+  return p;
+}
+
+void alloc_weights(tc_instance* I) {
+  const tc_model_dims& m = I->d;
+  const int64_t dm = m.d_model, H = m.n_heads, Hk = m.n_kv_heads, dh = m.head_dim, F = m.ffn_dim, V = m.vocab;
+  I->qkv_n = (int)((H + 2 * Hk) * dh);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t per_layer = al(I->qkv_n * dm * 2) + al(dm * H * dh * 2) + al(2 * F * dm * 2) + al(dm * F * 2) +
+                     al(I->qkv_n * 2) + 2 * al(dm * 2);
+  size_t total = 2 * al(V * dm * 2) + al(dm * 2) + per_layer * m.n_layers;
+  TC_CUDA(cudaMalloc(&I->weight_block, total));
+  uint8_t* cur = static_cast<uint8_t*>(I->weight_block);
+  cudaStream_t s = I->stream;
+  const uint64_t seed = I->desc.weight_seed;
+  I->embed = (__nv_bfloat16*)carve(cur, V * dm * 2);
+  init_tensor(I->embed, V, dm, seed, kTidEmbed, 1.0f, 0.f, 0, s);
+  I->lm_head.ptr = (__nv_bfloat16*)carve(cur, V * dm * 2);
+  I->lm_head.rows = V;
+  I->lm_head.cols = dm;
+  init_tensor(I->lm_head.ptr, V, dm, seed, kTidLmHead, kLinScale, 0.f, 0, s);
+  I->final_norm = (__nv_bfloat16*)carve(cur, dm * 2);
+  init_tensor(I->final_norm, 1, dm, seed, kTidFinalNorm, kNormScale, 1.f, 0, s);
+  I->layers.resize(m.n_layers);
+  for (int l = 0; l < m.n_layers; ++l) {
+    LayerW& L = I->layers[l];
+    L.qkv = {(__nv_bfloat16*)carve(cur, I->qkv_n * dm * 2), I->qkv_n, dm};
+    init_tensor(L.qkv.ptr, I->qkv_n, dm, seed, tid_layer(l, 0), kLinScale, 0.f, 0, s);
+    L.o = {(__nv_bfloat16*)carve(cur, dm * H * dh * 2), dm, H * dh};
+    init_tensor(L.o.ptr, dm, H * dh, seed, tid_layer(l, 1), kLinScale, 0.f, 0, s);
+    L.gate_up = {(__nv_bfloat16*)carve(cur, 2 * F * dm * 2), 2 * F, dm};
+    init_tensor(L.gate_up.ptr, 2 * F, dm, seed, tid_layer(l, 2), kLinScale, 0.f, 1, s);
+    L.down = {(__nv_bfloat16*)carve(cur, dm * F * 2), dm, F};
+    init_tensor(L.down.ptr, dm, F, seed, tid_layer(l, 4), kLinScale, 0.f, 0, s);
+    L.qkv_bias = (__nv_bfloat16*)carve(cur, I->qkv_n * 2);
+    init_tensor(L.qkv_bias, 1, I->qkv_n, seed, tid_layer(l, 7), m.qkv_bias ? kBiasScale : 0.f, 0.f, 0, s);
+    L.attn_norm = (__nv_bfloat16*)carve(cur, dm * 2);
+    init_tensor(L.attn_norm, 1, dm, seed, tid_layer(l, 5), kNormScale, 1.f, 0, s);
+    L.mlp_norm = (__nv_bfloat16*)carve(cur, dm * 2);
+    init_tensor(L.mlp_norm, 1, dm, seed, tid_layer(l, 6), kNormScale, 1.f, 0, s);
+    L.qkv.make_maps();
+    L.o.make_maps();
+    L.gate_up.make_maps();
+    L.down.make_maps();
+  }
+  I->lm_head.make_maps();
+}
+
+void alloc_buffers(tc_instance* I) {
+  const tc_model_dims& m = I->d;
+  const int T = I->desc.max_step_tokens, S = I->desc.max_seqs;
+  const int64_t dm = m.d_model;
+  // round row counts up to the GEMM M tile so TMA boxes never leave the buffer
+  const int Tp = (T + 127) / 128 * 128, Sp = (S + 127) / 128 * 128;
+  TC_CUDA(cudaMalloc(&I->resid, (size_t)Tp * dm * 4));
+  TC_CUDA(cudaMalloc(&I->xnorm, (size_t)Tp * dm * 2));
+  TC_CUDA(cudaMalloc(&I->qkv, (size_t)Tp * I->qkv_n * 2));
+  TC_CUDA(cudaMalloc(&I->attn_out, (size_t)Tp * m.n_heads * m.head_dim * 2));
+  TC_CUDA(cudaMalloc(&I->act, (size_t)Tp * m.ffn_dim * 2));
+  TC_CUDA(cudaMalloc(&I->lm_in, (size_t)Sp * dm * 2));
+  TC_CUDA(cudaMalloc(&I->logits, (size_t)S * m.vocab * 4));
+  TC_CUDA(cudaMalloc(&I->ids_dev, (size_t)S * 4));
+  TC_CUDA(cudaMallocHost(&I->ids_host, (size_t)S * 4));
+  TC_CUDA(cudaMemset(I->xnorm, 0, (size_t)Tp * dm * 2));
+  TC_CUDA(cudaMemset(I->attn_out, 0, (size_t)Tp * m.n_heads * m.head_dim * 2));
+  TC_CUDA(cudaMemset(I->act, 0, (size_t)Tp * m.ffn_dim * 2));
+  TC_CUDA(cudaMemset(I->lm_in, 0, (size_t)Sp * dm * 2));
+  I->map_xnorm = make_kmajor_map(I->xnorm, Tp, dm, 128);
+  I->map_attn = make_kmajor_map(I->attn_out, Tp, (uint64_t)m.n_heads * m.head_dim, 128);
+  I->map_act = make_kmajor_map(I->act, Tp, m.ffn_dim, 128);
+  I->map_lm_in = make_kmajor_map(I->lm_in, Sp, dm, 128);
+  // split-K partials: enough for the small-M weight-streaming regime (M <= 256)
+  I->splitk_floats = (size_t)std::min(T, 256) * std::max<int64_t>(2 * m.ffn_dim, m.vocab) * 4;
+  TC_CUDA(cudaMalloc(&I->splitk_ws, I->splitk_floats * 4));
+  // decode split-KV partials
+  const int G = m.n_heads / m.n_kv_heads;
+  const int max_splits = 64;
+  I->attn_ws_floats = (size_t)S * m.n_kv_heads * max_splits * G * m.head_dim;
+  TC_CUDA(cudaMalloc(&I->attn_ws_o, I->attn_ws_floats * 4));
+  TC_CUDA(cudaMalloc(&I->attn_ws_ml, (size_t)S * m.n_kv_heads * max_splits * G * 2 * 4));
+  // RoPE table in fp64 -> fp32
+  const int half = m.head_dim / 2;
+  std::vector<float2> cs((size_t)I->desc.max_context * half);
+  for (int pos = 0; pos < I->desc.max_context; ++pos)
+    for (int j = 0; j < half; ++j) {
+      const double inv = std::pow((double)m.rope_theta, -2.0 * j / (double)m.head_dim);
+      const double a = (double)pos * inv;
+      cs[(size_t)pos * half + j] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  TC_CUDA(cudaMalloc(&I->rope, cs.size() * sizeof(float2)));
+  TC_CUDA(cudaMemcpy(I->rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  // metadata: 3T + 4S + qblocks(<= T + S) * 2 + S (dec) + S (logit rows) + block tables
+  const int64_t max_pages_per_seq = (I->desc.max_context + I->desc.page_size - 1) / I->desc.page_size;
+  I->meta_ints = 3 * (size_t)T + 4 * (size_t)S + 2 * (size_t)(T + S) + 2 * (size_t)S +
+                 (size_t)S * max_pages_per_seq + 64;
+  TC_CUDA(cudaMallocHost(&I->meta_host, I->meta_ints * 4));
+  TC_CUDA(cudaMalloc(&I->meta_dev, I->meta_ints * 4));
+  TC_CUDA(cudaEventCreate(&I->ev_start));
+  TC_CUDA(cudaEventCreate(&I->ev_stop));
+  TC_CUDA(cudaEventCreate(&I->mig_a));
+  TC_CUDA(cudaEventCreate(&I->mig_b));
+  I->mig_cap = (int)(2 * max_pages_per_seq + 16);
+  TC_CUDA(cudaMallocHost(&I->mig_host, (size_t)I->mig_cap * 4));
+  TC_CUDA(cudaMalloc(&I->mig_dev, (size_t)I->mig_cap * 4));
+}
+
+void ensure_pages(tc_instance* I, int64_t req, int64_t n_tokens) {
+  const int ps = I->desc.page_size;
+  const int64_t need = (n_tokens + ps - 1) / ps;
+  std::vector<int32_t>& t = I->tables[req];
+  if ((int64_t)t.size() >= need) return;
+  if ((int64_t)I->free_pages.size() < need - (int64_t)t.size())
+    throw TcFail{TC_ERR_OOM, "KV pool exhausted (req " + std::to_string(req) + ", need " + std::to_string(need) +
+                                 " pages, free " + std::to_string(I->free_pages.size()) + ")"};
+  while ((int64_t)t.size() < need) {
+    t.push_back(I->free_pages.back());
+    I->free_pages.pop_back();
+  }
+}
+
+void release_pages(tc_instance* I, int64_t req) {
+  auto it = I->tables.find(req);
+  if (it == I->tables.end()) return;
+  for (auto p = it->second.rbegin(); p != it->second.rend(); ++p) I->free_pages.push_back(*p);
+  I->tables.erase(it);
+}
+
+struct ProfScope {
+  tc_instance* I;
+  cudaEvent_t b = nullptr;
+  const char* name;
+  ProfScope(tc_instance* inst, const char* n) : I(inst), name(n) {
+    if (I->prof.on) {
+      b = I->prof.get();
+      cudaEventRecord(b, I->stream);
+    }
+  }
+  ~ProfScope() {
+    if (I->prof.on) {
+      cudaEvent_t e = I->prof.get();
+      cudaEventRecord(e, I->stream);
+      I->prof.marks.push_back({name, {b, e}});
+    }
+  }
+};
+
+template <int DH, int G>
+void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec) {
+  const int hk = I->d.n_kv_heads;
+  if (n_qblk > 0) {
+    const int smem = 2 * tc::AttnTile<DH>::kStageElems * 2;
+    tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kAttnThreads, smem, I->stream>>>(p);
+    ++I->launches;
+  }
+  if (n_dec > 0) {
+    const int smem = 3 * tc::AttnTile<DH>::kStageElems * 2;
+    tc::attn_decode<DH, G><<<dim3(n_dec, hk, p.n_splits), tc::kAttnThreads, smem, I->stream>>>(p);
+    ++I->launches;
+    if (p.n_splits > 1) {
+      tc::attn_decode_combine<DH, G><<<dim3(n_dec, I->d.n_heads), DH, 0, I->stream>>>(p);
+      ++I->launches;
+    }
+  }
+  TC_CUDA(cudaGetLastError());
+}
+
+void dispatch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec) {
+  const int G = I->d.n_heads / I->d.n_kv_heads;
+  if (I->d.head_dim == 64 && G == 2) launch_attention<64, 2>(I, p, n_qblk, n_dec);
+  else if (I->d.head_dim == 128 && G == 4) launch_attention<128, 4>(I, p, n_qblk, n_dec);
+  else if (I->d.head_dim == 128 && G == 5) launch_attention<128, 5>(I, p, n_qblk, n_dec);
+  else throw TcFail{TC_ERR_INVALID, "unsupported attention shape"};
+}
+
+void step_launch(tc_instance* I, const tc_step_desc* st) {
+  TC_REQUIRE(st != nullptr, "step: null descriptor");
+  TC_REQUIRE(!I->step_pending, "step: previous step not waited");
+  const tc_model_dims& m = I->d;
+  const int ps = I->desc.page_size;
+  const int n_pf = st->n_prefill, n_dec = st->n_decode;
+  TC_REQUIRE(n_pf >= 0 && n_dec >= 0 && n_pf + n_dec > 0, "step: empty step");
+  const int n_seq = n_pf + n_dec;
+  TC_REQUIRE(n_seq <= I->desc.max_seqs, "step: too many sequences");
+  int T = n_dec;
+  for (int i = 0; i < n_pf; ++i) {
+    TC_REQUIRE(st->prefill[i].n_tokens >= 1 && st->prefill[i].pos0 >= 0, "step: bad prefill slice");
+    TC_REQUIRE(st->prefill[i].pos0 + st->prefill[i].n_tokens <= I->desc.max_context, "step: slice beyond max_context");
+    T += st->prefill[i].n_tokens;
+  }
+  TC_REQUIRE(T <= I->desc.max_step_tokens, "step: too many tokens");
+  for (int i = 0; i < n_dec; ++i)
+    TC_REQUIRE(st->decode[i].pos >= 0 && st->decode[i].pos < I->desc.max_context, "step: bad decode position");
+  // physical pages for every new position
+  for (int i = 0; i < n_pf; ++i) ensure_pages(I, st->prefill[i].req_id, st->prefill[i].pos0 + st->prefill[i].n_tokens);
+  for (int i = 0; i < n_dec; ++i) ensure_pages(I, st->decode[i].req_id, st->decode[i].pos + 1);
+
+  const int G = m.n_heads / m.n_kv_heads;
+  const int tpc = 4 * (16 / G);  // prefill tokens per attention CTA
+  int n_qblk = 0, n_logit = 0, n_bt = 0;
+  for (int i = 0; i < n_pf; ++i) {
+    n_qblk += (st->prefill[i].n_tokens + tpc - 1) / tpc;
+    n_logit += st->prefill[i].want_logits ? 1 : 0;
+    n_bt += (st->prefill[i].pos0 + st->prefill[i].n_tokens + ps - 1) / ps;
+  }
+  n_logit += n_dec;
+  for (int i = 0; i < n_dec; ++i) n_bt += st->decode[i].pos / ps + 1;
+  // layout of the metadata block
+  int32_t* h = I->meta_host;
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    const size_t o = off;
+    off += (n + 3) & ~size_t(3);
+    return o;
+  };
+  const size_t o_tok = take(T), o_pos = take(T), o_rseq = take(T), o_qs = take(n_seq), o_ql = take(n_seq),
+               o_p0 = take(n_seq), o_bo = take(n_seq), o_qbs = take(n_qblk), o_qbo = take(n_qblk), o_dseq = take(n_dec),
+               o_lrow = take(n_logit), o_bt = take(n_bt);
+  TC_REQUIRE(off <= I->meta_ints, "step: metadata overflow");
+  int row = 0, qb = 0, lr = 0, bt = 0, max_tiles = 0;
+  for (int i = 0; i < n_pf; ++i) {
+    const tc_prefill_slice& sl = st->prefill[i];
+    const std::vector<int32_t>& pages = I->tables[sl.req_id];
+    h[o_qs + i] = row;
+    h[o_ql + i] = sl.n_tokens;
+    h[o_p0 + i] = sl.pos0;
+    h[o_bo + i] = bt;
+    const int np = (sl.pos0 + sl.n_tokens + ps - 1) / ps;
+    for (int k = 0; k < np; ++k) h[o_bt + bt++] = pages[k];
+    for (int k = 0; k < sl.n_tokens; ++k) {
+      const int32_t tok = sl.token_ids[k];
+      TC_REQUIRE(tok >= 0 && tok < m.vocab, "step: token id out of range");
+      h[o_tok + row + k] = tok;
+      h[o_pos + row + k] = sl.pos0 + k;
+      h[o_rseq + row + k] = i;
+    }
+    for (int q = 0; q < sl.n_tokens; q += tpc) {
+      h[o_qbs + qb] = i;
+      h[o_qbo + qb] = q;
+      ++qb;
+    }
+    row += sl.n_tokens;
+    if (sl.want_logits) h[o_lrow + lr++] = row - 1;
+  }
+  for (int j = 0; j < n_dec; ++j) {
+    const tc_decode_item& di = st->decode[j];
+    const int s = n_pf + j;
+    const std::vector<int32_t>& pages = I->tables[di.req_id];
+    TC_REQUIRE(di.token_id >= 0 && di.token_id < m.vocab, "step: token id out of range");
+    h[o_qs + s] = row;
+    h[o_ql + s] = 1;
+    h[o_p0 + s] = di.pos;
+    h[o_bo + s] = bt;
+    const int np = di.pos / ps + 1;
+    for (int k = 0; k < np; ++k) h[o_bt + bt++] = pages[k];
+    h[o_tok + row] = di.token_id;
+    h[o_pos + row] = di.pos;
+    h[o_rseq + row] = s;
+    h[o_dseq + j] = s;
+    h[o_lrow + lr++] = row;
+    max_tiles = std::max(max_tiles, (di.pos + 1 + tc::kAttnKeys - 1) / tc::kAttnKeys);
+    ++row;
+  }
+  cudaStream_t s = I->stream;
+  DeviceGuard dg(I->desc.device);
+  if (I->prof.on) I->prof.reset();
+  I->launches = 0;
+  I->h2d_bytes = (int64_t)off * 4;
+  TC_CUDA(cudaEventRecord(I->ev_start, s));
+  TC_CUDA(cudaMemcpyAsync(I->meta_dev, h, off * 4, cudaMemcpyHostToDevice, s));
+  const int32_t* dm = I->meta_dev;
+
+  // decode split-KV: enough CTAs to cover ~2 waves of the SMs
+  int splits = 1, tps = std::max(1, max_tiles);
+  if (n_dec > 0) {
+    const int base = n_dec * m.n_kv_heads;
+    splits = std::min(std::max(1, (2 * I->sms + base - 1) / base), std::max(1, max_tiles));
+    splits = std::min(splits, 64);
+    tps = (max_tiles + splits - 1) / splits;
+    splits = (max_tiles + tps - 1) / tps;
+  }
+
+  {
+    ProfScope ps_(I, "embed");
+    tc::embed_rows<<<T, 256, 0, s>>>(dm + o_tok, I->embed, I->resid, m.d_model);
+    ++I->launches;
+  }
+  tc::AttnParams ap{};
+  ap.qkv = I->qkv;
+  ap.out = I->attn_out;
+  ap.kv = I->kv;
+  ap.page_stride = I->page_elems;
+  ap.n_layers = m.n_layers;
+  ap.n_heads = m.n_heads;
+  ap.n_kv_heads = m.n_kv_heads;
+  ap.page_size = ps;
+  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m.head_dim));
+  ap.seq_q_start = dm + o_qs;
+  ap.seq_q_len = dm + o_ql;
+  ap.seq_pos0 = dm + o_p0;
+  ap.seq_bt_off = dm + o_bo;
+  ap.block_tables = dm + o_bt;
+  ap.qblk_seq = dm + o_qbs;
+  ap.qblk_off = dm + o_qbo;
+  ap.dec_seq = dm + o_dseq;
+  ap.n_splits = splits;
+  ap.tiles_per_split = tps;
+  ap.ws_o = I->attn_ws_o;
+  ap.ws_ml = I->attn_ws_ml;
+  tc::RopeAppendParams rp{};
+  rp.qkv = I->qkv;
+  rp.kv = I->kv;
+  rp.rope_cs = I->rope;
+  rp.positions = dm + o_pos;
+  rp.row_seq = dm + o_rseq;
+  rp.seq_bt_off = dm + o_bo;
+  rp.block_tables = dm + o_bt;
+  rp.page_stride = I->page_elems;
+  rp.n_heads = m.n_heads;
+  rp.n_kv_heads = m.n_kv_heads;
+  rp.head_dim = m.head_dim;
+  rp.page_size = ps;
+  const int rms_threads = 256;
+  for (int l = 0; l < m.n_layers; ++l) {
+    const LayerW& L = I->layers[l];
+    {
+      ProfScope p_(I, "norm");
+      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps);
+      ++I->launches;
+    }
+    {
+      ProfScope p_(I, "gemm_qkv");
+      I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, L.qkv_bias, m.qkv_bias ? tc::EPI_BF16_BIAS : tc::EPI_BF16,
+               I->sms, I->splitk_ws, I->splitk_floats, s);
+    }
+    {
+      ProfScope p_(I, "rope_append");
+      rp.layer = l;
+      tc::rope_kv_append<<<T, 128, 0, s>>>(rp);
+      ++I->launches;
+    }
+    {
+      ProfScope p_(I, "attn");
+      ap.layer = l;
+      dispatch_attention(I, ap, n_qblk, n_dec);
+    }
+    {
+      ProfScope p_(I, "gemm_o");
+      I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->splitk_ws,
+               I->splitk_floats, s);
+    }
+    {
+      ProfScope p_(I, "norm");
+      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps);
+      ++I->launches;
+    }
+    {
+      ProfScope p_(I, "gemm_gate_up");
+      I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->splitk_ws,
+               I->splitk_floats, s);
+    }
+    {
+      ProfScope p_(I, "gemm_down");
+      I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->splitk_ws,
+               I->splitk_floats, s);
+    }
+  }
+  if (n_logit > 0) {
+    ProfScope p_(I, "lm_head");
+    tc::rmsnorm_rows<rms_threads><<<n_logit, rms_threads, 0, s>>>(I->resid, dm + o_lrow, I->final_norm, I->lm_in,
+                                                                  m.d_model, m.rms_eps);
+    I->launches += 2;  // gathered RMSNorm + argmax
+    I->launches += run_gemm(I->map_lm_in, I->lm_head, n_logit, I->logits, m.vocab, nullptr, tc::EPI_F32, I->sms, I->splitk_ws,
+             I->splitk_floats, s);
+    tc::argmax_rows<1024><<<n_logit, 1024, 0, s>>>(I->logits, m.vocab, I->ids_dev);
+    TC_CUDA(cudaMemcpyAsync(I->ids_host, I->ids_dev, (size_t)n_logit * 4, cudaMemcpyDeviceToHost, s));
+  }
+  TC_CUDA(cudaGetLastError());
+  TC_CUDA(cudaEventRecord(I->ev_stop, s));
+  I->step_pending = true;
+  I->last_sampled = n_logit;
+}
+
+void step_wait(tc_instance* I, tc_step_result* r) {
+  TC_REQUIRE(I->step_pending, "wait: no step in flight");
+  DeviceGuard dg(I->desc.device);
+  TC_CUDA(cudaEventSynchronize(I->ev_stop));
+  I->step_pending = false;
+  if (!r) return;
+  r->n_sampled = I->last_sampled;
+  r->launches = I->launches;
+  r->h2d_bytes = I->h2d_bytes;
+  r->d2h_bytes = (int64_t)I->last_sampled * 4 + (r->logits ? (int64_t)I->last_sampled * I->d.vocab * 4 : 0);
+  if (r->sampled_ids) std::memcpy(r->sampled_ids, I->ids_host, (size_t)I->last_sampled * 4);
+  if (r->logits && I->last_sampled > 0)
+    TC_CUDA(cudaMemcpy(r->logits, I->logits, (size_t)I->last_sampled * I->d.vocab * 4, cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  TC_CUDA(cudaEventElapsedTime(&ms, I->ev_start, I->ev_stop));
+  r->gpu_ms = ms;
+}
+
+void destroy(tc_instance* I) {
+  DeviceGuard dg(I->desc.device);
+  if (I->stream) cudaStreamSynchronize(I->stream);
+  auto f = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  f(I->weight_block); f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
+  f(I->logits); f(I->ids_dev); f(I->splitk_ws); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->rope); f(I->meta_dev);
+  f(I->mig_dev);
+  if (I->ids_host) cudaFreeHost(I->ids_host);
+  if (I->meta_host) cudaFreeHost(I->meta_host);
+  if (I->mig_host) cudaFreeHost(I->mig_host);
+  for (cudaEvent_t e : {I->ev_start, I->ev_stop, I->mig_a, I->mig_b})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : I->prof.pool) cudaEventDestroy(e);
+  if (I->stream) cudaStreamDestroy(I->stream);
+  delete I;
+}
+
+void enable_peer(int a, int b) {
+  if (a == b) return;
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({a, b})) return;
+  int can = 0;
+  TC_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+  TC_REQUIRE(can, "peer access unavailable between GPUs " + std::to_string(a) + " and " + std::to_string(b));
+  DeviceGuard g(a);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) TC_CUDA(e);
+  cudaGetLastError();
+  done.insert({a, b});
+}
+
+void migrate(tc_instance* src, tc_instance* dst, int64_t req, int64_t n_tokens) {
+  TC_REQUIRE(src && dst && src != dst, "migrate: need two distinct instances");
+  TC_REQUIRE(src->page_elems == dst->page_elems && src->desc.page_size == dst->desc.page_size,
+             "migrate: instances differ in KV geometry");
+  TC_REQUIRE(!src->mig_pending, "migrate: previous migration on this source not waited");
+  auto it = src->tables.find(req);
+  TC_REQUIRE(it != src->tables.end(), "migrate: request has no KV on source");
+  TC_REQUIRE(dst->tables.find(req) == dst->tables.end() || dst->tables[req].empty(),
+             "migrate: request already has KV on destination");
+  const int ps = src->desc.page_size;
+  const int64_t np = (n_tokens + ps - 1) / ps;
+  TC_REQUIRE(np <= (int64_t)it->second.size(), "migrate: source holds fewer pages than requested");
+  TC_REQUIRE(2 * np <= src->mig_cap, "migrate: request too long");
+  ensure_pages(dst, req, n_tokens);
+  const std::vector<int32_t>& dp = dst->tables[req];
+  for (int64_t i = 0; i < np; ++i) {
+    src->mig_host[i] = it->second[i];
+    src->mig_host[np + i] = dp[i];
+  }
+  enable_peer(src->desc.device, dst->desc.device);
+  DeviceGuard dg(src->desc.device);
+  cudaStream_t s = src->stream;
+  TC_CUDA(cudaMemcpyAsync(src->mig_dev, src->mig_host, (size_t)2 * np * 4, cudaMemcpyHostToDevice, s));
+  TC_CUDA(cudaEventRecord(src->mig_a, s));
+  const int64_t page_vec = src->page_elems * 2 / 16;
+  const int blocks = (int)std::min<int64_t>(2 * src->sms, std::max<int64_t>(1, np * page_vec / (512 * 4)));
+  if (np > 0)
+    tc::kv_copy_pages<<<blocks, 512, 0, s>>>(reinterpret_cast<const uint4*>(src->kv), reinterpret_cast<uint4*>(dst->kv),
+                                             src->mig_dev, src->mig_dev + np, (int)np, page_vec);
+  TC_CUDA(cudaGetLastError());
+  TC_CUDA(cudaEventRecord(src->mig_b, s));
+  // destination's next step must see the copied pages
+  TC_CUDA(cudaStreamWaitEvent(dst->stream, src->mig_b, 0));
+  // pages become reusable on the source once the copy is ordered on its stream
+  release_pages(src, req);
+  src->mig_pending = true;
+  src->mig_bytes = np * src->page_elems * 2;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* tc_last_error(void) { return g_last_error.c_str(); }
+const char* tc_version(void) { return "taichi_b200 0.1 (sm_100a)"; }
+
+tc_status tc_model_preset(const char* name, tc_model_dims* out) {
+  return guarded([&] {
+    TC_REQUIRE(name && out, "preset: null argument");
+    *out = preset(name);
+  });
+}
+
+uint16_t tc_weight_value(uint64_t seed, uint64_t tensor_id, int64_t index, float scale, float offset) {
+  const uint64_t key = tc::sm64(seed ^ tc::sm64(tensor_id));
+  const uint64_t h = tc::sm64(key + (uint64_t)index);
+  const float u = (float)(uint32_t)(h >> 40) * 5.9604644775390625e-08f;
+  const float c = u * 2.0f - 1.0f;
+  volatile float prod = c * scale;  // keep the two roundings separate
+  const float v = prod + offset;
+  uint32_t bits;
+  std::memcpy(&bits, &v, 4);
+  const uint32_t lsb = (bits >> 16) & 1u;
+  return (uint16_t)((bits + 0x7FFFu + lsb) >> 16);
+}
+
+tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
+  tc_instance* I = nullptr;
+  const tc_status st = guarded([&] {
+    TC_REQUIRE(desc && out, "create: null argument");
+    check_dims(desc->dims);
+    TC_REQUIRE(desc->page_size == 16, "create: page_size must be 16");
+    TC_REQUIRE(desc->max_step_tokens >= 1 && desc->max_seqs >= 1 && desc->max_context >= 16, "create: bad limits");
+    TC_REQUIRE(desc->kv_pool_tokens >= desc->page_size, "create: KV pool too small");
+    I = new tc_instance();
+    I->desc = *desc;
+    I->d = desc->dims;
+    int n_dev = 0;
+    TC_CUDA(cudaGetDeviceCount(&n_dev));
+    TC_REQUIRE(desc->device >= 0 && desc->device < n_dev, "create: no such CUDA device");
+    DeviceGuard dg(desc->device);
+    int major = 0, minor = 0;
+    TC_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, desc->device));
+    TC_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, desc->device));
+    TC_REQUIRE(major == 10 && minor == 0, "create: libtaichi_b200 is built for sm_100a (B200) only");
+    I->sms = device_sms(desc->device);
+    init_kernel_attrs(desc->device);
+    TC_CUDA(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+    alloc_weights(I);
+    alloc_buffers(I);
+    const tc_model_dims& m = I->d;
+    I->page_elems = (int64_t)m.n_layers * 2 * m.n_kv_heads * desc->page_size * m.head_dim;
+    I->n_pages = (desc->kv_pool_tokens + desc->page_size - 1) / desc->page_size;
+    TC_CUDA(cudaMalloc(&I->kv, (size_t)I->n_pages * I->page_elems * 2));
+    TC_CUDA(cudaMemsetAsync(I->kv, 0, (size_t)I->n_pages * I->page_elems * 2, I->stream));
+    I->free_pages.resize(I->n_pages);
+    for (int64_t i = 0; i < I->n_pages; ++i) I->free_pages[i] = (int32_t)(I->n_pages - 1 - i);  // pop_back -> 0,1,..
+    TC_CUDA(cudaStreamSynchronize(I->stream));
+  });
+  if (st != TC_OK) {
+    if (I) destroy(I);
+    return st;
+  }
+  *out = I;
+  return TC_OK;
+}
+
+tc_status tc_instance_destroy(tc_instance* inst) {
+  return guarded([&] {
+    if (inst) destroy(inst);
+  });
+}
+
+tc_status tc_step_launch(tc_instance* inst, const tc_step_desc* step) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "step: null instance");
+    step_launch(inst, step);
+  });
+}
+
+tc_status tc_step_wait(tc_instance* inst, tc_step_result* result) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "wait: null instance");
+    step_wait(inst, result);
+  });
+}
+
+tc_status tc_kv_reserve(tc_instance* inst, int64_t req_id, int64_t n_tokens) {
+  return guarded([&] {
+    TC_REQUIRE(inst && n_tokens >= 0, "reserve: bad argument");
+    ensure_pages(inst, req_id, n_tokens);
+  });
+}
+
+tc_status tc_kv_release(tc_instance* inst, int64_t req_id) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "release: null instance");
+    release_pages(inst, req_id);
+  });
+}
+
+tc_status tc_kv_stats(tc_instance* inst, int64_t req_id, int64_t* req_pages, int64_t* free_pages) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "stats: null instance");
+    auto it = inst->tables.find(req_id);
+    if (req_pages) *req_pages = it == inst->tables.end() ? 0 : (int64_t)it->second.size();
+    if (free_pages) *free_pages = (int64_t)inst->free_pages.size();
+  });
+}
+
+tc_status tc_kv_migrate(tc_instance* src, tc_instance* dst, int64_t req_id, int64_t n_tokens) {
+  return guarded([&] { migrate(src, dst, req_id, n_tokens); });
+}
+
+tc_status tc_kv_migrate_wait(tc_instance* src, float* copy_ms, int64_t* bytes) {
+  return guarded([&] {
+    TC_REQUIRE(src && src->mig_pending, "migrate_wait: no migration in flight");
+    DeviceGuard dg(src->desc.device);
+    TC_CUDA(cudaEventSynchronize(src->mig_b));
+    float ms = 0.f;
+    TC_CUDA(cudaEventElapsedTime(&ms, src->mig_a, src->mig_b));
+    if (copy_ms) *copy_ms = ms;
+    if (bytes) *bytes = src->mig_bytes;
+    src->mig_pending = false;
+  });
+}
+
+tc_status tc_kv_pool_info(tc_instance* inst, void** base, int64_t* page_bytes, int64_t* n_pages) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "pool_info: null instance");
+    if (base) *base = inst->kv;
+    if (page_bytes) *page_bytes = inst->page_elems * 2;
+    if (n_pages) *n_pages = inst->n_pages;
+  });
+}
+
+tc_status tc_kv_pages(tc_instance* inst, int64_t req_id, int32_t* pages, int32_t max_pages, int32_t* n_pages) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "pages: null instance");
+    auto it = inst->tables.find(req_id);
+    const int32_t n = it == inst->tables.end() ? 0 : (int32_t)it->second.size();
+    if (n_pages) *n_pages = n;
+    for (int32_t i = 0; i < n && i < max_pages && pages; ++i) pages[i] = it->second[i];
+  });
+}
+
+tc_status tc_weight_ptr(tc_instance* inst, const char* name, void** ptr, int64_t* rows, int64_t* cols) {
+  return guarded([&] {
+    TC_REQUIRE(inst && name && ptr, "weight_ptr: null argument");
+    const tc_model_dims& m = inst->d;
+    const std::string n = name;
+    auto put = [&](void* p, int64_t r, int64_t c) {
+      *ptr = p;
+      if (rows) *rows = r;
+      if (cols) *cols = c;
+    };
+    if (n == "embed") return put(inst->embed, m.vocab, m.d_model);
+    if (n == "lm_head") return put(inst->lm_head.ptr, m.vocab, m.d_model);
+    if (n == "final_norm") return put(inst->final_norm, 1, m.d_model);
+    TC_REQUIRE(n.size() > 1 && n[0] == 'L' && n.find('.') != std::string::npos, "weight_ptr: unknown weight " + n);
+    const int l = std::stoi(n.substr(1, n.find('.') - 1));
+    TC_REQUIRE(l >= 0 && l < m.n_layers, "weight_ptr: layer out of range");
+    const std::string f = n.substr(n.find('.') + 1);
+    const LayerW& L = inst->layers[l];
+    if (f == "qkv") return put(L.qkv.ptr, L.qkv.rows, L.qkv.cols);
+    if (f == "o") return put(L.o.ptr, L.o.rows, L.o.cols);
+    if (f == "gate_up") return put(L.gate_up.ptr, L.gate_up.rows, L.gate_up.cols);
+    if (f == "down") return put(L.down.ptr, L.down.rows, L.down.cols);
+    if (f == "qkv_bias") return put(L.qkv_bias, 1, inst->qkv_n);
+    if (f == "attn_norm") return put(L.attn_norm, 1, m.d_model);
+    if (f == "mlp_norm") return put(L.mlp_norm, 1, m.d_model);
+    throw TcFail{TC_ERR_INVALID, "weight_ptr: unknown weight " + n};
+  });
+}
+
+tc_status tc_gemm(int32_t device, const void* a, const void* b, void* out, const void* bias, int32_t m, int32_t n,
+                  int32_t k, int32_t epilogue, int32_t bn, int32_t k_splits, void* stream) {
+  return guarded([&] {
+    TC_REQUIRE(a && b && out && m > 0 && n > 0 && k > 0, "gemm: bad argument");
+    TC_REQUIRE(epilogue >= 0 && epilogue <= 4, "gemm: bad epilogue");
+    DeviceGuard dg(device);
+    init_kernel_attrs(device);
+    const int sms = device_sms(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    WMat w;
+    w.ptr = (__nv_bfloat16*)b;
+    w.rows = n;
+    w.cols = k;
+    w.make_maps();
+    const int mp = (m + 127) / 128 * 128;  // callers pass A with >= mp rows allocated? no: clamp the map to m rows
+    (void)mp;
+    const CUtensorMap am = make_kmajor_map(a, m, k, 128);
+    const int ldo = epilogue == tc::EPI_SWIGLU ? n / 2 : n;
+    float* ws = nullptr;
+    size_t ws_floats = 0;
+    if (k_splits != 1) {
+      GemmChoice c = choose_gemm(m, n, k, epilogue, sms, bn, k_splits, (size_t)1 << 40);
+      if (c.k_splits > 1) {
+        ws_floats = (size_t)c.k_splits * m * n;
+        TC_CUDA(cudaMallocAsync(&ws, ws_floats * 4, s));
+      }
+    }
+    run_gemm(am, w, m, out, ldo, (const __nv_bfloat16*)bias, epilogue, sms, ws, ws_floats, s, bn,
+             k_splits == 1 ? -1 : k_splits);
+    if (ws) TC_CUDA(cudaFreeAsync(ws, s));
+  });
+}
+
+tc_status tc_copy_pages(const void* src_pool, void* dst_pool, const int32_t* src_pages_dev,
+                        const int32_t* dst_pages_dev, int32_t n_pages, int64_t page_bytes, void* stream) {
+  return guarded([&] {
+    TC_REQUIRE(src_pool && dst_pool && n_pages >= 0 && page_bytes % 16 == 0, "copy_pages: bad argument");
+    if (n_pages == 0) return;
+    int dev = 0;
+    TC_CUDA(cudaGetDevice(&dev));
+    const int sms = device_sms(dev);
+    const int64_t page_vec = page_bytes / 16;
+    const int blocks = (int)std::min<int64_t>(2 * sms, std::max<int64_t>(1, n_pages * page_vec / (512 * 4)));
+    tc::kv_copy_pages<<<blocks, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const uint4*>(src_pool), reinterpret_cast<uint4*>(dst_pool), src_pages_dev, dst_pages_dev,
+        n_pages, page_vec);
+    TC_CUDA(cudaGetLastError());
+  });
+}
+
+tc_status tc_read_device(void* host_dst, const void* dev_src, size_t bytes) {
+  return guarded([&] {
+    TC_REQUIRE(host_dst && dev_src, "read_device: null argument");
+    TC_CUDA(cudaMemcpy(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+tc_status tc_set_profiling(tc_instance* inst, int32_t on) {
+  return guarded([&] {
+    TC_REQUIRE(inst, "profiling: null instance");
+    inst->prof.on = on != 0;
+  });
+}
+
+tc_status tc_phase_ms(tc_instance* inst, const char* phase, float* ms) {
+  return guarded([&] {
+    TC_REQUIRE(inst && phase && ms, "phase_ms: null argument");
+    DeviceGuard dg(inst->desc.device);
+    TC_CUDA(cudaEventSynchronize(inst->ev_stop));
+    float total = 0.f;
+    for (auto& mk : inst->prof.marks) {
+      if (mk.first != phase) continue;
+      float t = 0.f;
+      TC_CUDA(cudaEventElapsedTime(&t, mk.second.first, mk.second.second));
+      total += t;
+    }
+    *ms = total;
+  });
+}
+
+}  // extern "C"

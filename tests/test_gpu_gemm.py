@@ -1,0 +1,82 @@
+"""tcgen05 GEMM (csrc/gemm.cuh) through the C ABI (tc_gemm) vs a torch fp32 reference of the
+same bf16 operands. Tolerances: bf16 outputs rtol 1e-2 (one bf16 rounding, 2^-8) plus
+atol 1e-2 * std(ref); fp32 outputs rtol 1e-4, atol 1e-4 * std(ref) (accumulation order only)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+EPI_BF16, EPI_BIAS, EPI_RESID, EPI_SWIGLU, EPI_F32 = 0, 1, 2, 3, 4
+
+
+def _run(a, b, out, m, n, k, epi, bias=None, bn=0, splits=0):
+    from paper_2508_01989_b200 import runtime
+    runtime.gemm(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, k, epi,
+                 bias.data_ptr() if bias is not None else None, bn, splits)
+    torch.cuda.synchronize()
+
+
+def _close(got, ref, bf16_out):
+    s = ref.float().std().item() + 1e-6
+    if bf16_out:
+        torch.testing.assert_close(got.float(), ref, rtol=1e-2, atol=1e-2 * s)
+    else:
+        torch.testing.assert_close(got.float(), ref, rtol=1e-4, atol=1e-4 * s)
+
+
+@pytest.mark.parametrize("m,n,k,bn,splits", [
+    (128, 256, 64, 256, 1), (1, 256, 128, 0, 0), (100, 512, 256, 0, 0), (129, 1024, 512, 128, 1),
+    (576, 6144, 4096, 0, 0), (576, 4096, 4096, 0, 0), (64, 6144, 4096, 0, 0), (64, 4096, 14336, 0, 0),
+    (1100, 1024, 4096, 0, 0), (256, 512, 1024, 64, 1), (64, 512, 1024, 128, 4), (200, 256, 4096, 256, 2),
+])
+def test_gemm_bf16(cuda_ok, m, n, k, bn, splits):
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n + k)
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16, generator=g)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16, generator=g)
+    out = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
+    _run(a, b, out, m, n, k, EPI_BF16, bn=bn, splits=splits)
+    _close(out, a.float() @ b.float().T, True)
+
+
+@pytest.mark.parametrize("m,splits", [(37, 0), (300, 1), (64, 2)])
+def test_gemm_bias(cuda_ok, m, splits):
+    n, k = 7168, 5120
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.05
+    bias = torch.randn(n, device="cuda", dtype=torch.bfloat16)
+    out = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
+    _run(a, b, out, m, n, k, EPI_BIAS, bias=bias, splits=splits)
+    _close(out, a.float() @ b.float().T + bias.float(), True)
+
+
+@pytest.mark.parametrize("m,n,k,splits", [(576, 4096, 4096, 0), (64, 4096, 14336, 0), (17, 256, 512, 1),
+                                          (64, 4096, 4096, 4)])
+def test_gemm_residual_add(cuda_ok, m, n, k, splits):
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.02
+    resid = torch.randn(m, n, device="cuda", dtype=torch.float32)
+    ref = resid + a.float() @ b.float().T
+    _run(a, b, resid, m, n, k, EPI_RESID, splits=splits)
+    _close(resid, ref, False)
+
+
+@pytest.mark.parametrize("m,f,k,bn,splits", [(576, 14336, 4096, 0, 0), (64, 14336, 4096, 0, 0),
+                                             (33, 512, 256, 128, 1), (130, 1024, 512, 256, 1), (64, 512, 1024, 128, 2)])
+def test_gemm_swiglu_interleaved(cuda_ok, m, f, k, bn, splits):
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    wg = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
+    wu = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
+    phys = torch.stack([wg.view(f // 64, 64, k), wu.view(f // 64, 64, k)], dim=1).reshape(2 * f, k).contiguous()
+    out = torch.zeros(m, f, device="cuda", dtype=torch.bfloat16)
+    _run(a, phys, out, m, 2 * f, k, EPI_SWIGLU, bn=bn, splits=splits)
+    ref = torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T)
+    _close(out, ref, True)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 128256, 4096), (65, 128256, 4096), (130, 152064, 5120), (3, 1024, 256)])
+def test_gemm_f32_logits(cuda_ok, m, n, k):
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.03
+    out = torch.zeros(m, n, device="cuda", dtype=torch.float32)
+    _run(a, b, out, m, n, k, EPI_F32)
+    _close(out, a.float() @ b.float().T, False)

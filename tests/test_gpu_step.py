@@ -1,0 +1,237 @@
+"""The hybrid step through the C ABI (tc_step_launch / tc_step_wait) vs the CPU oracle
+(oracle/model_ref.py, parity UNPINNED -- see its header).
+
+Stated tolerances:
+  * logits: max |gpu - oracle| <= 0.05 * std(oracle logits) + 0.02 (bf16 storage points are
+    emulated by the oracle; remaining differences are fp32 accumulation order, bf16 rounding
+    of attention probabilities, exp2 approximations);
+  * greedy tokens: identical except at near-ties, where the oracle's top-2 gap < 0.02; after a
+    near-tie divergence the oracle continues from the GPU token (teacher forcing).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import model_ref as mr
+
+pytestmark = pytest.mark.gpu
+
+NEAR_TIE = 0.02
+
+
+def logit_tol(ref):
+    return 0.05 * float(ref.std()) + 0.02
+
+
+def check_logits(gpu, ref):
+    gpu = torch.as_tensor(gpu)
+    err = (gpu - ref).abs().max().item()
+    assert err <= logit_tol(ref), f"max |dlogit| {err:.4f} > {logit_tol(ref):.4f}"
+
+
+class Follower:
+    """Oracle decoder for one request, teacher-forced on GPU tokens at near-ties."""
+
+    def __init__(self, model, prompt):
+        self.model, self.cache, self.pos = model, model.new_cache(), 0
+        self.x = None
+        self.feed(prompt)
+        self.near_ties = 0
+
+    def feed(self, toks):
+        self.x = self.model.forward(list(toks), self.pos, self.cache)
+        self.pos += len(toks)
+
+    def check(self, gpu_token, gpu_logits=None):
+        lg = self.model.logits(self.x[-1:])[0]
+        if gpu_logits is not None:
+            check_logits(gpu_logits, lg)
+        top2 = torch.topk(lg, 2).values
+        ref_tok = int(torch.argmax(lg))
+        if ref_tok != gpu_token:
+            assert float(top2[0] - top2[1]) < NEAR_TIE, f"token mismatch {gpu_token} vs {ref_tok} (not a near-tie)"
+            self.near_ties += 1
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from paper_2508_01989_b200 import Instance
+    inst = Instance("tiny", weight_seed=11, kv_pool_tokens=1 << 15, max_step_tokens=2048, max_seqs=64,
+                    max_context=4096)
+    d = mr.preset("tiny")
+    model = mr.RefModel(d, mr.generate_weights(d, 11))
+    yield inst, model
+    inst.close()
+
+
+def test_tiny_weights_bitexact_with_oracle_init(tiny):
+    inst, model = tiny
+    d = mr.preset("tiny")
+    np.testing.assert_array_equal(inst.weight("L1.qkv"), mr.gen_bits(11, mr.tid_layer(1, 0), 512, 256, mr.LIN_SCALE, 0.0))
+    np.testing.assert_array_equal(inst.weight("embed"), mr.gen_bits(11, mr.TID_EMBED, d.vocab, d.d_model, np.float32(1), 0.0))
+    gu = inst.weight("L0.gate_up").reshape(d.ffn_dim // 64, 2, 64, d.d_model)
+    np.testing.assert_array_equal(gu[:, 1].reshape(d.ffn_dim, -1),
+                                  mr.gen_bits(11, mr.tid_layer(0, 3), d.ffn_dim, d.d_model, mr.LIN_SCALE, 0.0))
+
+
+def test_tiny_chunked_prefill_then_decode(tiny):
+    inst, model = tiny
+    rid = 1
+    prompt = mr.prompt_tokens(11, rid, 37, 1024)
+    inst.step(prefill=[(rid, 0, prompt[:16], False)])
+    out = inst.step(prefill=[(rid, 16, prompt[16:], True)], keep_logits=True)
+    f = Follower(model, prompt)
+    f.check(int(out.sampled[0]), out.logits[0])
+    tok, pos = int(out.sampled[0]), 37
+    for _ in range(12):
+        f.feed([tok])
+        out = inst.step(decode=[(rid, pos, tok)], keep_logits=True)
+        f.check(int(out.sampled[0]), out.logits[0])
+        tok, pos = int(out.sampled[0]), pos + 1
+    inst.kv_release(rid)
+
+
+def test_tiny_mixed_batches(tiny):
+    """Several requests at different phases share steps; a chunk spans two prompts."""
+    inst, model = tiny
+    rng = np.random.default_rng(5)
+    reqs = {}
+    for rid in range(10, 16):
+        n = int(rng.integers(5, 300))
+        reqs[rid] = {"prompt": mr.prompt_tokens(11, rid, n, 1024), "done": 0, "tok": None, "pos": 0}
+    followers = {}
+    chunk = 128
+    for it in range(60):
+        prefill, decode = [], []
+        budget = chunk
+        for rid, r in reqs.items():
+            if r["tok"] is not None:
+                decode.append((rid, r["pos"], r["tok"]))
+        for rid, r in reqs.items():
+            left = len(r["prompt"]) - r["done"]
+            if left > 0 and budget > 0:
+                take = min(left, budget)
+                prefill.append((rid, r["done"], r["prompt"][r["done"]:r["done"] + take], take == left))
+                budget -= take
+        if not prefill and not decode:
+            break
+        out = inst.step(prefill=prefill, decode=decode, keep_logits=True)
+        k = 0
+        for rid, pos0, toks, want in prefill:
+            reqs[rid]["done"] += len(toks)
+            if want:
+                r = reqs[rid]
+                followers[rid] = Follower(model, r["prompt"])
+                followers[rid].check(int(out.sampled[k]), out.logits[k])
+                r["tok"], r["pos"] = int(out.sampled[k]), len(r["prompt"])
+                k += 1
+        for rid, pos, tok in decode:
+            f = followers[rid]
+            f.feed([tok])
+            f.check(int(out.sampled[k]), out.logits[k])
+            reqs[rid]["tok"], reqs[rid]["pos"] = int(out.sampled[k]), pos + 1
+            k += 1
+    assert len(followers) == len(reqs)
+    for rid in reqs:
+        inst.kv_release(rid)
+
+
+def test_kv_pages_released_and_reused(tiny):
+    inst, _ = tiny
+    _, free0 = inst.kv_stats()
+    inst.step(prefill=[(99, 0, list(range(40)), True)])
+    n, free1 = inst.kv_stats(99)
+    assert n == 3 and free1 == free0 - 3
+    inst.kv_release(99)
+    assert inst.kv_stats(99) == (0, free0)
+
+
+def test_error_paths(tiny):
+    from paper_2508_01989_b200.runtime import TaichiError
+    inst, _ = tiny
+    with pytest.raises(TaichiError, match="token id out of range"):
+        inst.step(prefill=[(5, 0, [5000], True)])
+    with pytest.raises(TaichiError, match="empty step"):
+        inst.step()
+    inst.kv_release(5)
+
+
+def test_tiny_migration_between_instances(tiny):
+    """Init-style migration (P-heavy -> D-heavy) on one GPU: pages are byte-identical and the
+    destination continues the exact greedy trajectory."""
+    from paper_2508_01989_b200 import Instance
+    src, model = tiny
+    dst = Instance("tiny", weight_seed=11, kv_pool_tokens=1 << 14, max_step_tokens=512, max_seqs=16, max_context=4096)
+    rid = 77
+    prompt = mr.prompt_tokens(11, rid, 150, 1024)
+    out = src.step(prefill=[(rid, 0, prompt, True)])
+    src_pages = src.kv_pages(rid)
+    before = src.read_pages(src_pages)
+    src.migrate_to(dst, rid, len(prompt))
+    ms, nbytes = src.migrate_wait()
+    assert src.kv_stats(rid)[0] == 0
+    dst_pages = dst.kv_pages(rid)
+    assert len(dst_pages) == len(src_pages) and nbytes == len(src_pages) * before.shape[1]
+    np.testing.assert_array_equal(dst.read_pages(dst_pages), before)
+    f = Follower(model, prompt)
+    f.check(int(out.sampled[0]))
+    tok, pos = int(out.sampled[0]), len(prompt)
+    for _ in range(6):
+        f.feed([tok])
+        o = dst.step(decode=[(rid, pos, tok)], keep_logits=True)
+        f.check(int(o.sampled[0]), o.logits[0])
+        tok, pos = int(o.sampled[0]), pos + 1
+    dst.close()
+
+
+@pytest.fixture(scope="module")
+def llama_l2():
+    from paper_2508_01989_b200 import Instance
+    inst = Instance("llama3_8b:L2", weight_seed=3, kv_pool_tokens=1 << 15, max_step_tokens=1024, max_seqs=64,
+                    max_context=8192)
+    d = mr.preset("llama3_8b:L2")
+    model = mr.RefModel(d, mr.weights_from_device(inst, d), max_pos=8192)
+    yield inst, model
+    inst.close()
+
+
+def test_llama_shape_prefill_decode_long_context(llama_l2):
+    """Llama-3-8B layer shapes (2 layers): 1000-token prompt in 512 chunks, then split-KV decode."""
+    inst, model = llama_l2
+    rid = 5
+    prompt = mr.prompt_tokens(3, rid, 1000, 128256)
+    inst.step(prefill=[(rid, 0, prompt[:512], False)])
+    out = inst.step(prefill=[(rid, 512, prompt[512:], True)], keep_logits=True)
+    f = Follower(model, prompt)
+    f.check(int(out.sampled[0]), out.logits[0])
+    tok, pos = int(out.sampled[0]), 1000
+    for _ in range(4):
+        f.feed([tok])
+        o = inst.step(decode=[(rid, pos, tok)], keep_logits=True)
+        f.check(int(o.sampled[0]), o.logits[0])
+        tok, pos = int(o.sampled[0]), pos + 1
+    inst.kv_release(rid)
+
+
+def test_llama_shape_mixed_step(llama_l2):
+    """One step = a prefill chunk spanning two prompts + 20 decodes (M = 150 rows)."""
+    inst, model = llama_l2
+    prompts = {rid: mr.prompt_tokens(3, rid, 40 + 3 * rid, 128256) for rid in range(100, 120)}
+    follow = {}
+    toks = {}
+    for rid, p in prompts.items():
+        o = inst.step(prefill=[(rid, 0, p, True)])
+        toks[rid] = int(o.sampled[0])
+        follow[rid] = Follower(model, p)
+        follow[rid].check(toks[rid])
+    a = mr.prompt_tokens(3, 500, 70, 128256)
+    b = mr.prompt_tokens(3, 501, 60, 128256)
+    decode = [(rid, len(p), toks[rid]) for rid, p in prompts.items()]
+    out = inst.step(prefill=[(500, 0, a, True), (501, 0, b[:40], False)], decode=decode, keep_logits=True)
+    fa = Follower(model, a)
+    fa.check(int(out.sampled[0]), out.logits[0])
+    for k, (rid, pos, tok) in enumerate(decode):
+        follow[rid].feed([tok])
+        follow[rid].check(int(out.sampled[1 + k]), out.logits[1 + k])
+    for rid in list(prompts) + [500, 501]:
+        inst.kv_release(rid)
