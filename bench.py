@@ -1,0 +1,289 @@
+#!/usr/bin/env python3
+"""bench.py -- hybrid-step throughput of the B200 TaiChi instance (BASELINE.json config 2).
+
+Workload (N=1): one aggregated Llama-3-8B-shaped instance (random-init bf16 weights,
+synthetic token ids), chunk size 512. One "step" = one hybrid iteration: a 512-token
+prefill chunk of a 1024-token prompt (positions 512..1023, so it attends to a 512-token
+paged prefix) piggybacked with 64 decode requests at context 1024 -- T = 576 rows through
+32 layers + LM head on the 65 sampled rows + greedy argmax. Weights (15 GB) and the KV
+cache (8.6 GB of decode context) are far larger than L2 (126 MB), so no flush is needed.
+
+  value     tokens/s from device time (CUDA events on the instance stream, inputs resident)
+  e2e       tokens/s through the C ABI (tc_step_launch / tc_step_wait) with host token ids in
+            and sampled ids out, wall clock around the step loop
+  roofline  the dominant kernel (gate_up GEMM, fused SwiGLU) vs measured bf16 tensor peak
+  cpu_baseline  the oracle port of the same step in torch fp32 on the host cores (1 layer,
+            scaled to 32)
+
+N>1 (torchrun): every rank drives its own instance on its own GPU (independent TaiChi
+instances; the step has no collective) -> "scaling": "weak", value = sum over ranks.
+--impl reference: the CPU implementation (oracle port) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+
+def step_cost(d, P, prefix, D, ctx, n_logit):
+    """Algorithmic flops / bytes per kernel class for one step."""
+    H, Hk, dh, dm, F, V, L = d["n_heads"], d["n_kv_heads"], d["head_dim"], d["d_model"], d["ffn_dim"], d["vocab"], d["n_layers"]
+    T = P + D
+    qkv_n = (H + 2 * Hk) * dh
+    kv_tok = 2 * Hk * dh * 2  # bytes of K+V per token per layer
+    k = {}
+    def gemm(name, m, n, kk):
+        k[name] = {"flops": 2.0 * m * n * kk * L, "bytes": (n * kk * 2 + m * kk * 2 + m * n * 2) * L}
+    gemm("gemm_qkv", T, qkv_n, dm)
+    gemm("gemm_o", T, dm, H * dh)
+    gemm("gemm_gate_up", T, 2 * F, dm)
+    gemm("gemm_down", T, dm, F)
+    pairs_p = P * prefix + P * (P + 1) // 2
+    pairs_d = D * (ctx + 1)
+    k["attn"] = {"flops": 4.0 * H * dh * (pairs_p + pairs_d) * L,
+                 "bytes": ((prefix + P) + D * (ctx + 1)) * kv_tok * L + T * (qkv_n + H * dh) * 2 * L}
+    k["lm_head"] = {"flops": 2.0 * n_logit * V * dm, "bytes": V * dm * 2 + n_logit * V * 4}
+    k["elementwise"] = {"flops": 0.0, "bytes": T * dm * (4 + 2) * 2 * L * 2}
+    return k
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = [r.split(", ") for r in pathlib.Path(self.f.name).read_text().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for i, n in enumerate(names):
+                if len(r) >= 9 and r[5 + i].strip() == "Active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def measured_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return j["hbm_gbs"], j["bf16_tflops"], j["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=1):
+    from oracle import cpu_step, model_ref as mr
+    import torch
+    d = mr.Dims(**dims)
+    threads = os.cpu_count() or 1
+    sec, det = cpu_step.time_step(d, P, prefix, D, ctx, n_logit, repeats=repeats, threads=threads)
+    return {"value": (P + D) / sec, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"1 of {d.n_layers} layers of the same step (P={P} prefix={prefix} D={D} ctx={ctx}) + LM head on "
+                      f"{n_logit} rows, torch fp32, best of {repeats}; step time = layer*{d.n_layers} + head",
+            "seconds_per_step": sec, **det}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama3_8b")
+    ap.add_argument("--prefill", type=int, default=512)
+    ap.add_argument("--prefix", type=int, default=512)
+    ap.add_argument("--decode", type=int, default=64)
+    ap.add_argument("--ctx", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-window", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off)")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    P, prefix, D, ctx = args.prefill, args.prefix, args.decode, args.ctx
+    n_logit = D + 1
+    workload = (f"{args.model} hybrid step: {P}-token prefill chunk (prefix {prefix}) + {D} decodes @ ctx {ctx}; "
+                f"chunk size 512, single aggregated instance per GPU")
+    config = {"workload": workload, "model_shape": args.model, "step_rows": P + D, "prefill_tokens": P,
+              "prefill_prefix": prefix, "decode_reqs": D, "decode_ctx": ctx, "instances": world,
+              "l2": "inputs larger than L2 (15 GB weights + 8.6 GB KV per step), no flush needed"}
+    metric = "hybrid-step tokens/s"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import cpu_step, model_ref as mr
+        import torch
+        d = mr.preset(args.model)
+        cs = cpu_step.CpuStep(d, P, prefix, D, ctx, n_logit, threads=os.cpu_count())
+        vals = []
+        for i in range(args.warmup + args.steps):
+            sec_i, det = cs.run()
+            if i >= args.warmup:
+                vals.append(sec_i)
+        sec = statistics.median(vals)
+        v = (P + D) / sec
+        cb = {"value": v, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+              "sample": f"per step: 1 of {d.n_layers} layers of the same step + LM head on {n_logit} rows, torch "
+                        f"fp32, scaled to {d.n_layers} layers; median of {args.steps} steps after {args.warmup} warm-up",
+              "seconds_per_step": sec}
+        print(json.dumps({"metric": metric, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "config": config, "impl": "reference", "cpu_baseline": cb,
+                          "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2508_01989_b200 import Instance
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    inst = Instance(args.model, device=dev, weight_seed=1, kv_pool_tokens=(D + 2) * (ctx + 64) + prefix + P + 4096,
+                    max_step_tokens=max(P + D, 512), max_seqs=D + 8, max_context=max(ctx, prefix + P) + 64)
+    dims = inst.dims.as_dict()
+    V = dims["vocab"]
+    import numpy as np
+    rng = np.random.default_rng(1000 + rank)
+    # setup (untimed): prefill the chunk's prefix and every decode context
+    prompt = rng.integers(0, V, prefix + P).tolist()
+    if prefix:
+        for s in range(0, prefix, 512):
+            inst.step(prefill=[(0, s, prompt[s:min(prefix, s + 512)], False)])
+    for rid in range(1, D + 1):
+        toks = rng.integers(0, V, ctx).tolist()
+        for s in range(0, ctx, 512):
+            inst.step(prefill=[(rid, s, toks[s:s + 512], False)])
+    dec_tok = rng.integers(0, V, D).tolist()
+    step_prefill = [(0, prefix, prompt[prefix:prefix + P], True)] if P else []
+    step_decode = [(rid, ctx, dec_tok[rid - 1]) for rid in range(1, D + 1)]
+
+    def one_step():
+        return inst.step(prefill=step_prefill, decode=step_decode)
+
+    for _ in range(args.warmup):
+        one_step()
+    # timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    gpu_ms, launches, h2d, d2h = [], 0, 0, 0
+    if args.profile_window:
+        torch.cuda.profiler.start()
+    with ClockSampler(dev) as clocks:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            o = one_step()
+            gpu_ms.append(o.gpu_ms)
+            launches += o.launches
+            h2d, d2h = o.h2d_bytes, o.d2h_bytes
+        t1 = time.perf_counter()
+    torch.cuda.synchronize(dev)
+    if args.profile_window:
+        torch.cuda.profiler.stop()
+    dev_s, wall_s = sum(gpu_ms) / 1e3, t1 - t0
+    if world > 1:
+        t = torch.tensor([dev_s, wall_s], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s, wall_s = t.tolist()
+        dist.barrier()
+    tokens = (P + D) * args.steps * world
+    value = tokens / dev_s
+    e2e = tokens / wall_s
+
+    # per-phase device times (separate pass with per-kernel events) -> dominant-kernel roofline
+    inst.set_profiling(True)
+    phases = {}
+    prof_steps = max(3, min(args.steps, 5))
+    prof_step_ms = []
+    for _ in range(prof_steps):
+        o = one_step()
+        prof_step_ms.append(o.gpu_ms)
+        for ph in ["gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "attn", "rope_append", "norm", "lm_head", "embed"]:
+            phases.setdefault(ph, []).append(inst.phase_ms(ph))
+    inst.set_profiling(False)
+    phases = {k: statistics.median(v) for k, v in phases.items()}
+    hbm, peak, peak_sus, peak_kind = measured_peaks()
+    cost = step_cost(dims, P, prefix, D, ctx, n_logit)
+    L = dims["n_layers"]
+    gu = cost["gemm_gate_up"]
+    gu_launch_s = phases["gemm_gate_up"] / 1e3 / L
+    achieved = gu["flops"] / L / gu_launch_s / 1e12
+    traffic = None
+    tf = REPO / "profiles" / "gemm_gate_up_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "kernel": "gemm_gate_up (tcgen05, fused SwiGLU)", "achieved": achieved,
+                "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus, "traffic": traffic,
+                "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
+                "flops_per_launch": gu["flops"] / L, "avg_launch_ms": gu_launch_s * 1e3,
+                "share_of_step": phases["gemm_gate_up"] / statistics.median(prof_step_ms)}
+    # whole-step roofline: sum over kernel classes of max(F/peak, B/BW) vs the step time
+    bound_s = sum(max(c["flops"] / (peak_sus * 1e12), c["bytes"] / (hbm * 1e9)) for c in cost.values())
+    step_ms = dev_s / args.steps * 1e3 if world == 1 else statistics.median(gpu_ms)
+    step_roofline = {"bound_ms": bound_s * 1e3, "measured_ms": step_ms, "frac": bound_s * 1e3 / step_ms,
+                     "phase_ms": phases, "profiled_step_ms": statistics.median(prof_step_ms),
+                     "kernels": {k: {"flops": v["flops"], "bytes": v["bytes"],
+                                     "bound_ms": 1e3 * max(v["flops"] / (peak_sus * 1e12), v["bytes"] / (hbm * 1e9)),
+                                     "measured_ms": phases.get(k)} for k, v in cost.items()}}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=1)
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random token ids)",
+                "config": config, "clocks": clocks.summary(),
+                "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches * world, "roofline": roofline, "step_roofline": step_roofline,
+                "cpu_baseline": cb}
+        print(json.dumps(line))
+    inst.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

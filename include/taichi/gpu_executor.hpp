@@ -1,0 +1,173 @@
+// GpuExecutor -- the pdsim::StepExecutor that runs the engine's decisions on B200s
+// through the C ABI (include/taichi_b200.h). One tc_instance per TaiChi instance.
+//
+//   launch_step      BatchPlan -> tc_step_desc: prefill slices carry synthetic prompt ids
+//                    (splitmix64(seed ^ rid << 20 ^ pos) % vocab; traces are lengths only,
+//                    types.hpp:28-31), decode rows feed each request's last token.
+//   complete_step    tc_step_wait; sampled ids are held until the engine commits them.
+//   token_committed  appends the held token to the request's output.
+//   start_transfer   tc_kv_migrate of the rows physically written: prompt_len for Init,
+//                    footprint-1 for degrade/backflow (the newest token is not fed yet).
+//   request_done     tc_kv_release.
+//
+// Clock modes: Logical returns the cost-model price (schedule bit-exact with the
+// reference; the GPU runs asynchronously and is joined at completion), Wall returns the
+// measured device time of the step / copy (SLO metrics from real B200 execution).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "pdsim/engine.hpp"
+#include "pdsim/rng.hpp"
+#include "taichi_b200.h"
+
+namespace taichi {
+
+enum class ClockMode { Logical, Wall };
+
+inline void tc_check(tc_status s, const char* what) {
+  if (s == TC_OK) return;
+  const std::string msg = std::string(what) + ": " + tc_last_error();
+  if (s == TC_ERR_INVALID) throw pdsim::ConfigError(msg);
+  throw pdsim::EngineError(msg);
+}
+
+inline int32_t synth_token(std::uint64_t seed, std::int64_t rid, std::int64_t pos, int32_t vocab) {
+  const std::uint64_t idx = (seed ^ (static_cast<std::uint64_t>(rid) << 20)) ^ static_cast<std::uint64_t>(pos);
+  return static_cast<int32_t>(pdsim::splitmix64(idx) % static_cast<std::uint64_t>(vocab));
+}
+
+struct ExecStats {
+  long long steps = 0, migrations = 0;
+  double step_gpu_ms = 0.0, copy_ms = 0.0;
+  long long copy_bytes = 0, launches = 0;
+};
+
+class GpuExecutor final : public pdsim::StepExecutor {
+ public:
+  GpuExecutor(std::vector<tc_instance*> instances, std::vector<pdsim::TraceRecord> records, int32_t vocab,
+              std::uint64_t token_seed, ClockMode mode)
+      : inst_(std::move(instances)), recs_(std::move(records)), vocab_(vocab), seed_(token_seed), mode_(mode) {
+    reqs_.resize(recs_.size());
+    held_.resize(inst_.size());
+    order_.resize(inst_.size());
+    inflight_.assign(inst_.size(), false);
+  }
+
+  const std::vector<int32_t>& tokens(pdsim::RequestId rid) const { return reqs_[static_cast<size_t>(rid)].out; }
+  const ExecStats& stats() const { return stats_; }
+
+  double launch_step(pdsim::InstanceId i, const pdsim::BatchPlan& plan, double, double model_ms) override {
+    slices_.clear();
+    decodes_.clear();
+    ids_.clear();
+    std::size_t total = 0;
+    for (const auto& sl : plan.prefill_slices) total += static_cast<std::size_t>(sl.second);
+    ids_.reserve(total);
+    for (const auto& sl : plan.prefill_slices) {
+      Req& r = req(sl.first);
+      const std::int64_t pos0 = r.prefilled;
+      for (std::int64_t p = pos0; p < pos0 + sl.second; ++p) ids_.push_back(synth_token(seed_, sl.first, p, vocab_));
+      r.prefilled += sl.second;
+      const bool last = r.prefilled == recs_[static_cast<size_t>(sl.first)].prompt_len;
+      slices_.push_back(tc_prefill_slice{sl.first, static_cast<int32_t>(pos0), static_cast<int32_t>(sl.second),
+                                         nullptr, last ? 1 : 0});
+    }
+    std::size_t off = 0;
+    for (auto& s : slices_) {
+      s.token_ids = ids_.data() + off;
+      off += static_cast<std::size_t>(s.n_tokens);
+    }
+    for (pdsim::RequestId rid : plan.decode_reqs) {
+      const Req& r = req(rid);
+      const auto pos = recs_[static_cast<size_t>(rid)].prompt_len + static_cast<std::int64_t>(r.out.size()) - 1;
+      decodes_.push_back(tc_decode_item{rid, static_cast<int32_t>(pos), r.out.back()});
+    }
+    auto& order = order_[static_cast<size_t>(i)];  // sampled-id order: finishing prompts, then decodes
+    order.clear();
+    for (const auto& s : slices_)
+      if (s.want_logits) order.push_back(s.req_id);
+    for (const auto& dd : decodes_) order.push_back(dd.req_id);
+    tc_step_desc d{static_cast<int32_t>(slices_.size()), slices_.data(), static_cast<int32_t>(decodes_.size()),
+                   decodes_.data(), 0};
+    tc_check(tc_step_launch(inst_[static_cast<size_t>(i)], &d), "tc_step_launch");
+    inflight_[static_cast<size_t>(i)] = true;
+    ++stats_.steps;
+    if (mode_ == ClockMode::Logical) return model_ms;
+    const float ms = join(i);
+    return static_cast<double>(ms);
+  }
+
+  void complete_step(pdsim::InstanceId i, const pdsim::BatchPlan&, double) override {
+    if (inflight_[static_cast<size_t>(i)]) join(i);
+  }
+
+  void token_committed(pdsim::RequestId rid, pdsim::InstanceId i) override {
+    auto& held = held_[static_cast<size_t>(i)];
+    auto it = held.find(rid);
+    if (it == held.end()) throw pdsim::EngineError("token_committed: no sampled token for request");
+    req(rid).out.push_back(it->second);
+    held.erase(it);
+  }
+
+  double start_transfer(pdsim::RequestId rid, pdsim::InstanceId from, pdsim::InstanceId to, pdsim::Tokens tokens,
+                        pdsim::MigrationReason why, double, double model_ms) override {
+    // physically written KV rows: the whole prompt for Init; footprint - 1 otherwise
+    const std::int64_t rows = why == pdsim::MigrationReason::Init ? tokens : tokens - 1;
+    tc_instance* src = inst_[static_cast<size_t>(from)];
+    tc_check(tc_kv_migrate(src, inst_[static_cast<size_t>(to)], rid, rows), "tc_kv_migrate");
+    float ms = 0.f;
+    int64_t bytes = 0;
+    tc_check(tc_kv_migrate_wait(src, &ms, &bytes), "tc_kv_migrate_wait");
+    ++stats_.migrations;
+    stats_.copy_ms += ms;
+    stats_.copy_bytes += bytes;
+    held_[static_cast<size_t>(from)].erase(rid);  // a token sampled mid-flight is discarded
+    return mode_ == ClockMode::Logical ? model_ms : static_cast<double>(ms);
+  }
+
+  void request_done(pdsim::RequestId rid, pdsim::InstanceId i) override {
+    tc_check(tc_kv_release(inst_[static_cast<size_t>(i)], rid), "tc_kv_release");
+  }
+
+ private:
+  struct Req {
+    std::int64_t prefilled = 0;
+    std::vector<int32_t> out;
+  };
+  Req& req(pdsim::RequestId rid) { return reqs_[static_cast<size_t>(rid)]; }
+
+  float join(pdsim::InstanceId i) {
+    const auto& order = order_[static_cast<size_t>(i)];
+    std::vector<int32_t> ids(order.size() + 1);
+    tc_step_result r{};
+    r.sampled_ids = ids.data();
+    tc_check(tc_step_wait(inst_[static_cast<size_t>(i)], &r), "tc_step_wait");
+    inflight_[static_cast<size_t>(i)] = false;
+    stats_.step_gpu_ms += r.gpu_ms;
+    stats_.launches += r.launches;
+    auto& held = held_[static_cast<size_t>(i)];
+    for (std::size_t k = 0; k < order.size() && k < static_cast<std::size_t>(r.n_sampled); ++k) held[order[k]] = ids[k];
+    return r.gpu_ms;
+  }
+
+  std::vector<tc_instance*> inst_;
+  std::vector<pdsim::TraceRecord> recs_;
+  int32_t vocab_;
+  std::uint64_t seed_;
+  ClockMode mode_;
+  std::vector<Req> reqs_;
+  std::vector<std::unordered_map<pdsim::RequestId, int32_t>> held_;
+  std::vector<bool> inflight_;
+  std::vector<std::vector<pdsim::RequestId>> order_;
+  std::vector<tc_prefill_slice> slices_;
+  std::vector<tc_decode_item> decodes_;
+  std::vector<int32_t> ids_;
+  ExecStats stats_;
+};
+
+}  // namespace taichi

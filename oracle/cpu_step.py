@@ -59,30 +59,36 @@ def _layer_forward(L, d, x, p_prefix_k, p_prefix_v, P, dec_k, dec_v):
     return x + (torch.nn.functional.silu(h @ L["gate"].T) * (h @ L["up"].T)) @ L["down"].T
 
 
-@torch.no_grad()
-def time_step(d, P: int, prefix: int, D: int, ctx: int, n_logit: int, repeats: int = 1, threads: int | None = None):
-    """Seconds for one full-depth step, measured on ONE layer (+ LM head on n_logit rows) and
-    scaled by n_layers. Returns (seconds_per_step, detail dict)."""
-    if threads:
-        torch.set_num_threads(threads)
-    L = _layer(d)
-    g = torch.Generator().manual_seed(1)
-    x = torch.randn(P + D, d.d_model, generator=g)
-    pk = torch.randn(prefix, d.n_kv_heads, d.head_dim, generator=g)
-    pv = torch.randn(prefix, d.n_kv_heads, d.head_dim, generator=g)
-    dk = torch.randn(D, ctx, d.n_kv_heads, d.head_dim, generator=g)
-    dv = torch.randn(D, ctx, d.n_kv_heads, d.head_dim, generator=g)
-    lm = torch.randn(d.vocab, d.d_model, generator=g) * 0.02
-    _layer_forward(L, d, x, pk, pv, P, dk, dv)  # warm-up
-    best_layer, best_head = float("inf"), float("inf")
-    for _ in range(repeats):
+class CpuStep:
+    """Builds one layer of the target shape + the LM head once; run() times one full-depth step
+    (one layer measured, scaled by n_layers, plus the LM head on n_logit rows)."""
+
+    def __init__(self, d, P: int, prefix: int, D: int, ctx: int, n_logit: int, threads: int | None = None):
+        if threads:
+            torch.set_num_threads(threads)
+        self.d, self.P, self.n_logit = d, P, n_logit
+        self.L = _layer(d)
+        g = torch.Generator().manual_seed(1)
+        self.x = torch.randn(P + D, d.d_model, generator=g)
+        self.pk = torch.randn(prefix, d.n_kv_heads, d.head_dim, generator=g)
+        self.pv = torch.randn(prefix, d.n_kv_heads, d.head_dim, generator=g)
+        self.dk = torch.randn(D, ctx, d.n_kv_heads, d.head_dim, generator=g)
+        self.dv = torch.randn(D, ctx, d.n_kv_heads, d.head_dim, generator=g)
+        self.lm = torch.randn(d.vocab, d.d_model, generator=g) * 0.02
+
+    @torch.no_grad()
+    def run(self):
         t0 = time.perf_counter()
-        y = _layer_forward(L, d, x, pk, pv, P, dk, dv)
+        y = _layer_forward(self.L, self.d, self.x, self.pk, self.pv, self.P, self.dk, self.dv)
         t1 = time.perf_counter()
-        lg = _rms(y[-n_logit:], L["n1"]) @ lm.T
-        _ = lg.argmax(-1)
+        _ = (_rms(y[-self.n_logit:], self.L["n1"]) @ self.lm.T).argmax(-1)
         t2 = time.perf_counter()
-        best_layer, best_head = min(best_layer, t1 - t0), min(best_head, t2 - t1)
-    total = best_layer * d.n_layers + best_head
-    return total, {"layer_s": best_layer, "head_s": best_head, "layers_timed": 1, "scaled_to": d.n_layers,
-                   "threads": torch.get_num_threads()}
+        return (t1 - t0) * self.d.n_layers + (t2 - t1), {"layer_s": t1 - t0, "head_s": t2 - t1}
+
+
+def time_step(d, P, prefix, D, ctx, n_logit, repeats: int = 1, threads: int | None = None):
+    """Best-of-`repeats` seconds per full-depth step (after one warm-up run)."""
+    cs = CpuStep(d, P, prefix, D, ctx, n_logit, threads)
+    cs.run()
+    best, det = min((cs.run() for _ in range(repeats)), key=lambda r: r[0])
+    return best, {**det, "layers_timed": 1, "scaled_to": d.n_layers, "threads": torch.get_num_threads()}

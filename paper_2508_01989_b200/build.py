@@ -67,6 +67,18 @@ def build_host(force: bool = False) -> pathlib.Path:
     return out
 
 
+def build_serve(force: bool = False) -> pathlib.Path:
+    """Host engine + GPU executor, linked against lib/libtaichi_b200.so (rpath $ORIGIN)."""
+    out = LIB / "taichi_serve"
+    so = build_cuda(force)
+    deps = list((INCLUDE / "pdsim").glob("*.hpp")) + list((INCLUDE / "taichi").glob("*.hpp")) + \
+        [CSRC / "taichi_serve.cpp", INCLUDE / "taichi_b200.h", so]
+    if force or _stale(out, deps):
+        _run([CXX, *HOST_FLAGS, "-Wall", "-Wextra", f"-I{INCLUDE}", f"-I{NLOHMANN}", CSRC / "taichi_serve.cpp",
+              "-o", out, f"-L{LIB}", "-ltaichi_b200", "-Wl,-rpath,$ORIGIN", "-pthread"])
+    return out
+
+
 def build_reftests(force: bool = False) -> list[pathlib.Path]:
     """Reference gtest sources (read from /root/reference, never copied) vs our headers."""
     src_dir = pathlib.Path("/root/reference/proj/tests")
@@ -103,6 +115,7 @@ def build_oracle() -> None:
 def build_all(force: bool = False) -> None:
     build_cuda(force)
     build_host(force)
+    build_serve(force)
     build_reftests(force)
     build_oracle()
 

@@ -1,0 +1,132 @@
+// taichi_serve -- the host engine (include/pdsim) driving B200 instances through the C ABI.
+//
+//   taichi_serve --config F [--seed S] [--model tiny|llama3_8b|qwen2_5_14b[:Ln]]
+//                [--devices 0,1,..] [--clock logical|wall] [--pool-tokens N]
+//                [--log OUT] [--tokens OUT.jsonl]
+//
+// --clock logical: the cost model prices every step/transfer (schedule byte-identical to the
+//   reference's, checked against the oracle log) while every step really runs on the GPU and
+//   every migration really copies KV pages; tokens are written per request for the oracle.
+// --clock wall: measured device step / copy times drive the clock (real SLO goodput).
+// Instances are placed round-robin on --devices (one per GPU in production; several may
+// share a GPU in tests).
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "pdsim/pdsim.hpp"
+#include "taichi/gpu_executor.hpp"
+#include "taichi/schedule_log.hpp"
+
+namespace {
+std::vector<int> parse_ints(const std::string& s) {
+  std::vector<int> v;
+  std::size_t p = 0;
+  while (p < s.size()) {
+    std::size_t c = s.find(',', p);
+    if (c == std::string::npos) c = s.size();
+    if (c > p) v.push_back(std::stoi(s.substr(p, c - p)));
+    p = c + 1;
+  }
+  return v;
+}
+}  // namespace
+
+int main(int argc, char** argv) {
+  using namespace pdsim;
+  std::string config, model = "tiny", devices = "0", clock = "logical", log, tokens_out;
+  long long seed = -1, pool_tokens = 0;
+  unsigned long long weight_seed = 1;
+  for (int i = 1; i + 1 < argc; i += 2) {
+    const std::string k = argv[i], v = argv[i + 1];
+    if (k == "--config") config = v;
+    else if (k == "--seed") seed = std::stoll(v);
+    else if (k == "--model") model = v;
+    else if (k == "--devices") devices = v;
+    else if (k == "--clock") clock = v;
+    else if (k == "--pool-tokens") pool_tokens = std::stoll(v);
+    else if (k == "--log") log = v;
+    else if (k == "--tokens") tokens_out = v;
+    else if (k == "--weight-seed") weight_seed = std::stoull(v);
+    else {
+      std::fprintf(stderr, "unknown flag %s\n", k.c_str());
+      return 2;
+    }
+  }
+  std::vector<tc_instance*> insts;
+  int rc = 0;
+  try {
+    if (config.empty()) throw ConfigError("--config is required");
+    const ExperimentConfig cfg = load_config(config);
+    const std::uint64_t s = seed >= 0 ? static_cast<std::uint64_t>(seed) : cfg.workload.spec.seed;
+    EngineInputs in = make_engine_inputs(cfg, make_stack(cfg.mode, cfg.policy, cfg.early_reject), cfg.cluster, s);
+    tc_model_dims dims{};
+    taichi::tc_check(tc_model_preset(model.c_str(), &dims), "tc_model_preset");
+    Tokens max_prompt = 0, max_ctx = 0;
+    std::vector<TraceRecord> recs;
+    for (const Arrival& a : in.arrivals) {
+      recs.push_back(a.record);
+      max_prompt = std::max(max_prompt, a.record.prompt_len);
+      max_ctx = std::max(max_ctx, a.record.prompt_len + a.record.output_len);
+    }
+    const std::vector<int> devs = parse_ints(devices);
+    if (devs.empty()) throw ConfigError("--devices: empty");
+    for (std::size_t i = 0; i < in.instances.size(); ++i) {
+      const InstanceSpec& sp = in.instances[i];
+      tc_instance_desc d{};
+      d.device = devs[i % devs.size()];
+      d.dims = dims;
+      d.weight_seed = weight_seed;  // every instance holds the same model replica
+      d.page_size = 16;
+      // physical pool = logical capacity x 1.5 headroom (in-flight prefill, pending, transfers) + a max context
+      d.kv_pool_tokens = pool_tokens > 0 ? pool_tokens : sp.kv_capacity * 3 / 2 + max_ctx + 1024;
+      d.max_step_tokens = static_cast<int32_t>(std::max<Tokens>(sp.chunk_size, 1) + 1024);
+      d.max_seqs = 1024;
+      d.max_context = static_cast<int32_t>(max_ctx + 16);
+      tc_instance* h = nullptr;
+      taichi::tc_check(tc_instance_create(&d, &h), "tc_instance_create");
+      insts.push_back(h);
+    }
+    taichi::GpuExecutor exec(insts, recs, dims.vocab, s, clock == "wall" ? taichi::ClockMode::Wall : taichi::ClockMode::Logical);
+    in.executor = &exec;
+    FILE* f = log.empty() ? nullptr : std::fopen(log.c_str(), "w");
+    long long plans = 0;
+    in.observer = [&](InstanceId i, double t, const BatchPlan& p, double dt) {
+      ++plans;
+      if (f) taichi::log_plan(f, i, t, p, dt);
+    };
+    const SimulationResult sim = run_simulation(in);
+    if (f) {
+      taichi::log_result(f, sim);
+      std::fclose(f);
+    }
+    if (!tokens_out.empty()) {
+      FILE* t = std::fopen(tokens_out.c_str(), "w");
+      for (std::size_t r = 0; r < recs.size(); ++r) {
+        std::fprintf(t, "{\"id\": %zu, \"prompt_len\": %lld, \"tokens\": [", r, (long long)recs[r].prompt_len);
+        const auto& tk = exec.tokens(static_cast<RequestId>(r));
+        for (std::size_t k = 0; k < tk.size(); ++k) std::fprintf(t, "%s%d", k ? ", " : "", tk[k]);
+        std::fprintf(t, "]}\n");
+      }
+      std::fclose(t);
+    }
+    const MetricsReport rep = build_report(sim, cfg.slo);
+    const taichi::ExecStats& st = exec.stats();
+    std::printf(
+        "{\"iterations\": %lld, \"requests\": %zu, \"attainment\": %.17g, \"p90_ttft_ms\": %.17g, "
+        "\"p90_tpot_ms\": %.17g, \"migrations_init\": %lld, \"migrations_degrade\": %lld, "
+        "\"migrations_backflow\": %lld, \"sim_end_ms\": %.17g, \"gpu_steps\": %lld, \"gpu_step_ms\": %.6f, "
+        "\"gpu_launches\": %lld, \"kv_copies\": %lld, \"kv_copy_ms\": %.6f, \"kv_copy_bytes\": %lld, \"clock\": \"%s\"}\n",
+        plans, sim.lifecycles.size(), rep.agg.attainment, rep.agg.p90_ttft_ms, rep.agg.p90_tpot_ms,
+        sim.migrations_init, sim.migrations_degrade, sim.migrations_backflow, sim.sim_end_ms, st.steps,
+        st.step_gpu_ms, st.launches, st.migrations, st.copy_ms, st.copy_bytes, clock.c_str());
+  } catch (const ConfigError& e) {
+    std::fprintf(stderr, "config error: %s\n", e.what());
+    rc = 1;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    rc = 2;
+  }
+  for (tc_instance* h : insts) tc_instance_destroy(h);
+  return rc;
+}
