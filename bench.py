@@ -240,7 +240,7 @@ def main():
     for _ in range(prof_steps):
         o = one_step()
         prof_step_ms.append(o.gpu_ms)
-        for ph in ["gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "attn", "rope_append", "norm", "lm_head", "embed"]:
+        for ph in ["gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "attn", "norm", "lm_head", "embed"]:
             phases.setdefault(ph, []).append(inst.phase_ms(ph))
     inst.set_profiling(False)
     phases = {k: statistics.median(v) for k, v in phases.items()}

@@ -1,18 +1,24 @@
 // Paged attention for the hybrid step (SURVEY.md 2, K1 + K2).
 //
 // KV pool layout (page-major so one request's KV migrates as whole pages):
-//   pool[page][layer][k|v][kv_head][slot 0..PS-1][head_dim]   (bf16)
-// One page of Llama-3-8B = 32 x 2 x 8 x 16 x 128 x 2 B = 2 MiB; the K (or V)
-// rows of one (page, layer, kv_head) are 4 KiB contiguous, read with 16 B
-// cp.async into padded shared-memory tiles of 64 keys (4 pages).
+//   pool[page][layer][k|v][kv_head][slot 0..PS-1][head_dim]   (bf16, PS = 16)
+// One (page, layer, k|v, kv_head) block is 16 rows x head_dim, 4 KiB contiguous for
+// head_dim 128. It is fetched by ONE TMA instruction through a 3-D tensor map
+// {64 dims, head_dim/64 halves, pool rows} with 128 B swizzle, which lands it in
+// shared memory bank-conflict free for ldmatrix (address = line*128 +
+// ((chunk ^ line) & 7) * 16). Completion is tracked with mbarrier transaction
+// counts, so no thread computes per-chunk gather addresses.
 //
-//  * attn_prefill  -- chunked-prefill queries (a chunk may span prompts; each
-//    slice is a sequence) attend causally to the paged prefix + in-chunk keys.
-//    CTA = (16/G tokens x G heads) x 4 warps of one GQA group; QK^T and PV on
-//    tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate), online softmax.
-//  * attn_decode   -- one query token per request; CTA = (request, kv_head,
-//    KV split); the 4 warps take interleaved 16-key pages of each 64-key tile,
-//    merged in shared memory, then across splits by attn_decode_combine.
+//  * attn_prefill  -- chunked-prefill queries (a chunk may span prompts; each slice
+//    is a sequence) attend causally to the paged prefix + in-chunk keys. CTA =
+//    (16/G tokens x G heads) x 4 consumer warps of one GQA group + 1 TMA producer
+//    warp; 64-key tiles (4 pages) in a 3-stage full/empty mbarrier ring. QK^T and
+//    PV on tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate), online softmax.
+//  * attn_decode   -- split-KV at warp granularity: a work item is (request,
+//    kv_head, run of pages); a persistent grid of independent warps walks its
+//    items with a private 4-stage page ring (each warp issues its own TMA loads
+//    S-1 pages ahead, across item boundaries). Multi-item requests are merged by
+//    attn_decode_combine.
 #pragma once
 
 #include "common.cuh"
@@ -22,24 +28,22 @@ namespace tc {
 struct AttnParams {
   const __nv_bfloat16* qkv;  // [T, (H + 2 Hkv) * DH], RoPE already applied to q and k
   __nv_bfloat16* out;        // [T, H * DH]
-  const __nv_bfloat16* kv;   // pool base (bf16)
-  long long page_stride;     // elements per page
   int layer, n_layers, n_heads, n_kv_heads, page_size;
   float scale_log2;          // log2(e) / sqrt(DH)
-  // sequences of this step
   const int* seq_q_start;    // first packed row
   const int* seq_q_len;      // rows (1 for decode)
   const int* seq_pos0;       // position of the first row
   const int* seq_bt_off;     // offset into block_tables
   const int* block_tables;   // flat page ids
-  // prefill work list
-  const int* qblk_seq;
+  const int* qblk_seq;       // prefill work list
   const int* qblk_off;
-  // decode work list
-  const int* dec_seq;        // decode index -> sequence index
-  int n_splits, tiles_per_split;
-  float* ws_o;               // [n_dec, Hkv, splits, G, DH]
-  float* ws_ml;              // [n_dec, Hkv, splits, G, 2]
+  const int4* dec_items;     // decode work: (seq, kvh | final << 16, page0, page1)
+  int n_items;
+  const int* dec_seq;        // decode index -> sequence
+  const int* dec_item_base;  // decode index -> first item; items (d, kvh, j) at base + kvh * chunks + j
+  const int* dec_chunks;     // decode index -> items per kv head
+  float* ws_o;               // [item][G][DH]
+  float* ws_ml;              // [item][G][2]
 };
 
 TC_DEVICE void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -59,50 +63,35 @@ TC_DEVICE void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
-TC_DEVICE void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int bytes = valid ? 16 : 0;  // zero-fill when invalid
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+TC_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
-TC_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-TC_DEVICE void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
+TC_DEVICE void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int kAttnKeys = 64;  // keys per shared-memory tile
-constexpr int kAttnThreads = 128;
+constexpr int kPage = 16;  // tokens per KV page (tc_instance_desc.page_size)
 
 template <int DH>
-struct AttnTile {
-  static constexpr int LD = DH + 8;                      // padded row: conflict-free ldmatrix
-  static constexpr int kHalfElems = kAttnKeys * LD;      // K or V
-  static constexpr int kStageElems = 2 * kHalfElems;
-  static constexpr int kChunksPerRow = DH / 8;           // 16 B chunks
+struct KvBlock {
+  static constexpr int kBytes = kPage * DH * 2;  // one (page, k|v, head) block
+  static constexpr int kHalves = DH / 64;
 };
 
-// Stage keys [key0, key0 + 64) of (layer, kv_head) into smem K|V; keys >= kv_len are zero-filled.
+// Swizzled smem address of (key, col) inside consecutive page blocks starting at base.
 template <int DH>
-TC_DEVICE void attn_load_tile(const AttnParams& p, const int* bt, int kvh, int key0, int kv_len, uint32_t smem_stage) {
-  using T = AttnTile<DH>;
-  const long long head_off = ((long long)(p.layer * 2) * p.n_kv_heads + kvh) * p.page_size * DH;
-  const long long v_off = (long long)p.n_kv_heads * p.page_size * DH;
-  constexpr int kChunks = kAttnKeys * T::kChunksPerRow;
-#pragma unroll
-  for (int i = threadIdx.x; i < kChunks; i += kAttnThreads) {
-    const int key = i / T::kChunksPerRow;
-    const int part = i % T::kChunksPerRow;
-    const int gk = key0 + key;
-    const bool valid = gk < kv_len;
-    const int page = valid ? bt[gk / p.page_size] : 0;
-    const __nv_bfloat16* src = p.kv + (long long)page * p.page_stride + head_off +
-                               (long long)(gk % p.page_size) * DH + part * 8;
-    const uint32_t dst = smem_stage + (uint32_t)(key * T::LD + part * 8) * 2;
-    cp_async16(dst, src, valid);
-    cp_async16(dst + T::kHalfElems * 2, src + v_off, valid);
-  }
+TC_DEVICE uint32_t kv_addr(uint32_t base, int key, int col) {
+  const int line = (key & (kPage - 1)) * KvBlock<DH>::kHalves + (col >> 6);
+  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + line * 128 + ((((col & 63) >> 3) ^ (line & 7)) << 4));
 }
 
-// Q fragment (A operand) for the warp's 16 rows: row r -> (token row_tok[r], head row_head[r]).
+// Pool row of (page, layer, k|v, head, slot 0) for the 3-D tensor map.
+TC_DEVICE int kv_row(const AttnParams& p, int page, int kv, int head) {
+  return (((page * p.n_layers + p.layer) * 2 + kv) * p.n_kv_heads + head) * kPage;
+}
+
+// Q fragment (A operand) of 16 rows: rows lo / hi -> (token, head).
 template <int DH>
 TC_DEVICE void attn_load_q(const AttnParams& p, int tok_lo, int head_lo, bool ok_lo, int tok_hi, int head_hi,
                            bool ok_hi, uint32_t (&qf)[DH / 16][4]) {
@@ -119,22 +108,19 @@ TC_DEVICE void attn_load_q(const AttnParams& p, int tok_lo, int head_lo, bool ok
   }
 }
 
-// S[16 x 8*NT] = Q K^T for keys [kbase, kbase + 8*NT) of the staged tile.
+// S[16 x 8*NT] = Q K^T for keys [kbase, kbase + 8*NT) of the staged K blocks.
 template <int DH, int NT>
 TC_DEVICE void attn_qk(const uint32_t (&qf)[DH / 16][4], uint32_t k_smem, int kbase, float (&s)[NT][4]) {
-  using T = AttnTile<DH>;
   const int lane = threadIdx.x % 32;
+  const int j = lane / 8, r = lane % 8;
 #pragma unroll
   for (int t = 0; t < NT; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
 #pragma unroll
   for (int ks = 0; ks < DH / 16; ++ks) {
 #pragma unroll
     for (int t = 0; t < NT; t += 2) {
-      const int j = lane / 8, r = lane % 8;
-      const int key = kbase + t * 8 + (j / 2) * 8 + r;
-      const int dim = ks * 16 + (j % 2) * 8;
       uint32_t b0, b1, b2, b3;
-      ldsm_x4(k_smem + (uint32_t)(key * T::LD + dim) * 2, b0, b1, b2, b3);
+      ldsm_x4(kv_addr<DH>(k_smem, kbase + t * 8 + (j / 2) * 8 + r, ks * 16 + (j % 2) * 8), b0, b1, b2, b3);
       mma_bf16_16816(s[t], qf[ks], b0, b1);
       mma_bf16_16816(s[t + 1], qf[ks], b2, b3);
     }
@@ -144,8 +130,8 @@ TC_DEVICE void attn_qk(const uint32_t (&qf)[DH / 16][4], uint32_t k_smem, int kb
 // O[16 x DH] += P[16 x 8*NT] V[keys kbase.., DH]
 template <int DH, int NT>
 TC_DEVICE void attn_pv(const float (&pr)[NT][4], uint32_t v_smem, int kbase, float (&o)[DH / 8][4]) {
-  using T = AttnTile<DH>;
   const int lane = threadIdx.x % 32;
+  const int j = lane / 8, r = lane % 8;
 #pragma unroll
   for (int kk = 0; kk < NT / 2; ++kk) {
     uint32_t a[4];
@@ -155,11 +141,8 @@ TC_DEVICE void attn_pv(const float (&pr)[NT][4], uint32_t v_smem, int kbase, flo
     a[3] = pack_bf16(pr[2 * kk + 1][2], pr[2 * kk + 1][3]);
 #pragma unroll
     for (int n = 0; n < DH / 8; n += 2) {
-      const int j = lane / 8, r = lane % 8;
-      const int key = kbase + kk * 16 + (j % 2) * 8 + r;
-      const int dim = n * 8 + (j / 2) * 8;
       uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(v_smem + (uint32_t)(key * T::LD + dim) * 2, b0, b1, b2, b3);
+      ldsm_x4_t(kv_addr<DH>(v_smem, kbase + kk * 16 + (j % 2) * 8 + r, n * 8 + (j / 2) * 8), b0, b1, b2, b3);
       mma_bf16_16816(o[n], a, b0, b1);
       mma_bf16_16816(o[n + 1], a, b2, b3);
     }
@@ -218,13 +201,25 @@ TC_DEVICE void attn_softmax_step(float (&s)[NT][4], int key0, int key_lim_lo, in
   }
 }
 
+// ============================================================== chunked prefill
+constexpr int kPrefillStages = 3;
+constexpr int kPrefillThreads = 160;  // 4 consumer warps + 1 TMA producer warp
+constexpr int kTilePages = 4;         // 64 keys per tile
+
+template <int DH>
+struct PrefillSmem {
+  static constexpr int kStageBytes = 2 * kTilePages * KvBlock<DH>::kBytes;  // K pages then V pages
+  static constexpr int kBytes = kPrefillStages * kStageBytes + 1024;
+};
+
 template <int DH, int G>
-__global__ void __launch_bounds__(kAttnThreads) attn_prefill(AttnParams p) {
-  using T = AttnTile<DH>;
+__global__ void __launch_bounds__(kPrefillThreads) attn_prefill(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   constexpr int TPW = 16 / G;  // tokens per warp
   constexpr int TPC = 4 * TPW;
-  extern __shared__ __align__(16) uint8_t attn_smem[];
-  const uint32_t sbase = smem_u32(attn_smem);
+  constexpr int kKeys = kTilePages * kPage;
+  extern __shared__ uint8_t attn_smem_raw[];
+  __shared__ uint64_t full_bar[kPrefillStages], empty_bar[kPrefillStages];
+  const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int seq = p.qblk_seq[blockIdx.x];
   const int qoff = p.qblk_off[blockIdx.x];
@@ -232,8 +227,41 @@ __global__ void __launch_bounds__(kAttnThreads) attn_prefill(AttnParams p) {
   const int q_start = p.seq_q_start[seq], q_len = p.seq_q_len[seq], pos0 = p.seq_pos0[seq];
   const int* bt = p.block_tables + p.seq_bt_off[seq];
   const int kv_end = pos0 + min(qoff + TPC, q_len);
+  const int n_tiles = (kv_end + kKeys - 1) / kKeys;
+  const int n_pages = (kv_end + kPage - 1) / kPage;
 
-  // rows of this warp: r -> token r / G, head r % G
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPrefillStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 4);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 4) {
+    // ---------------- TMA producer: 4 K blocks + 4 V blocks per tile
+    if (lane == 0) {
+      tma_prefetch_desc(&kv_map);
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % kPrefillStages;
+        mbar_wait(&empty_bar[st], ((t / kPrefillStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full_bar[st], PrefillSmem<DH>::kStageBytes);
+        const uint32_t dst = sbase + st * PrefillSmem<DH>::kStageBytes;
+#pragma unroll
+        for (int pg = 0; pg < kTilePages; ++pg) {
+          const int gp = t * kTilePages + pg;
+          const int page = bt[gp < n_pages ? gp : 0];  // beyond the sequence: any valid page, masked
+          tma_load_3d(dst + pg * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, 0, kv_row(p, page, 0, kvh));
+          tma_load_3d(dst + (kTilePages + pg) * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, 0,
+                      kv_row(p, page, 1, kvh));
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: rows of this warp: r -> token r / G, head r % G
   const int r_lo = lane / 4, r_hi = lane / 4 + 8;
   const int tl_lo = qoff + warp * TPW + r_lo / G, tl_hi = qoff + warp * TPW + r_hi / G;
   const bool ok_lo = r_lo < TPW * G && tl_lo < q_len;
@@ -241,8 +269,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_prefill(AttnParams p) {
   const int head_lo = kvh * G + r_lo % G, head_hi = kvh * G + r_hi % G;
   uint32_t qf[DH / 16][4];
   attn_load_q<DH>(p, q_start + (ok_lo ? tl_lo : 0), head_lo, ok_lo, q_start + (ok_hi ? tl_hi : 0), head_hi, ok_hi, qf);
-  // causal bound (exclusive): query at position pos0 + tl sees keys <= pos0 + tl
-  const int lim_lo = ok_lo ? pos0 + tl_lo + 1 : 0;
+  const int lim_lo = ok_lo ? pos0 + tl_lo + 1 : 0;  // causal: query at pos0+tl sees keys <= pos0+tl
   const int lim_hi = ok_hi ? pos0 + tl_hi + 1 : 0;
 
   float o[DH / 8][4];
@@ -250,23 +277,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_prefill(AttnParams p) {
   for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
 
-  const int n_tiles = (kv_end + kAttnKeys - 1) / kAttnKeys;
-  attn_load_tile<DH>(p, bt, kvh, 0, kv_end, sbase);
-  cp_async_commit();
   for (int t = 0; t < n_tiles; ++t) {
-    const uint32_t stage = sbase + (uint32_t)((t & 1) * T::kStageElems) * 2;
-    if (t + 1 < n_tiles)
-      attn_load_tile<DH>(p, bt, kvh, (t + 1) * kAttnKeys, kv_end, sbase + (uint32_t)(((t + 1) & 1) * T::kStageElems) * 2);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
+    const int st = t % kPrefillStages;
+    mbar_wait(&full_bar[st], (t / kPrefillStages) & 1);
+    const uint32_t k_smem = sbase + st * PrefillSmem<DH>::kStageBytes;
+    const uint32_t v_smem = k_smem + kTilePages * KvBlock<DH>::kBytes;
     float s[8][4];
-    attn_qk<DH, 8>(qf, stage, 0, s);
-    attn_softmax_step<DH, 8>(s, t * kAttnKeys, lim_lo, lim_hi, p.scale_log2, m, l, o);
-    attn_pv<DH, 8>(s, stage + T::kHalfElems * 2, 0, o);
-    __syncthreads();
+    attn_qk<DH, 8>(qf, k_smem, 0, s);
+    attn_softmax_step<DH, 8>(s, t * kKeys, lim_lo, lim_hi, p.scale_log2, m, l, o);
+    attn_pv<DH, 8>(s, v_smem, 0, o);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
   }
-  // normalise and store
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     l[h] += __shfl_xor_sync(0xffffffffu, l[h], 1);
@@ -287,117 +309,121 @@ __global__ void __launch_bounds__(kAttnThreads) attn_prefill(AttnParams p) {
   }
 }
 
+// ============================================================== decode
+constexpr int kDecodeStages = 3;
+constexpr int kDecodeWarps = 4;
+
+template <int DH>
+struct DecodeSmem {
+  static constexpr int kStageBytes = 2 * KvBlock<DH>::kBytes;  // one page: K block then V block
+  static constexpr int kWarpBytes = kDecodeStages * kStageBytes;
+  static constexpr int kBytes = kDecodeWarps * kWarpBytes + 1024;
+};
+
 template <int DH, int G>
-__global__ void __launch_bounds__(kAttnThreads) attn_decode(AttnParams p) {
-  using T = AttnTile<DH>;
-  extern __shared__ __align__(16) uint8_t attn_smem[];
-  const uint32_t sbase = smem_u32(attn_smem);
+__global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  extern __shared__ uint8_t attn_smem_raw[];
+  __shared__ uint64_t bars[kDecodeWarps][kDecodeStages];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int d = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
-  const int seq = p.dec_seq[d];
-  const int q_row = p.seq_q_start[seq];
-  const int kv_len = p.seq_pos0[seq] + 1;
-  const int* bt = p.block_tables + p.seq_bt_off[seq];
-  const int n_tiles_all = (kv_len + kAttnKeys - 1) / kAttnKeys;
-  const int t0 = split * p.tiles_per_split;
-  const int t1 = min(n_tiles_all, t0 + p.tiles_per_split);
+  const uint32_t wbase = ((smem_u32(attn_smem_raw) + 1023u) & ~1023u) + warp * DecodeSmem<DH>::kWarpBytes;
+  uint64_t* full = bars[warp];
+  if (lane == 0) {
+    for (int s = 0; s < kDecodeStages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+    tma_prefetch_desc(&kv_map);
+  }
+  __syncwarp();
+  const int n_warps = gridDim.x * kDecodeWarps;
+  const int gw = blockIdx.x * kDecodeWarps + warp;
+
+  // load cursor (lane 0): walks this warp's (item, page) stream S-1 pages ahead
+  int l_item = gw, l_page = -1, issued = 0;
+  auto issue_next = [&]() {
+    while (l_item < p.n_items) {
+      const int4 it = p.dec_items[l_item];
+      if (l_page < 0) l_page = it.z;
+      if (l_page < it.w) {
+        const int page = p.block_tables[p.seq_bt_off[it.x] + l_page];
+        const int kvh = it.y & 0xffff;
+        const int st = issued % kDecodeStages;
+        const uint32_t dst = wbase + st * DecodeSmem<DH>::kStageBytes;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&full[st], DecodeSmem<DH>::kStageBytes);
+        tma_load_3d(dst, &kv_map, &full[st], 0, 0, kv_row(p, page, 0, kvh));
+        tma_load_3d(dst + KvBlock<DH>::kBytes, &kv_map, &full[st], 0, 0, kv_row(p, page, 1, kvh));
+        ++issued;
+        ++l_page;
+        return;
+      }
+      l_item += n_warps;
+      l_page = -1;
+    }
+  };
+  if (lane == 0)
+    for (int k = 0; k < kDecodeStages - 1; ++k) issue_next();
 
   const int r_lo = lane / 4, r_hi = lane / 4 + 8;
   const bool ok_lo = r_lo < G, ok_hi = r_hi < G;
-  uint32_t qf[DH / 16][4];
-  attn_load_q<DH>(p, q_row, kvh * G + (ok_lo ? r_lo : 0), ok_lo, q_row, kvh * G + (ok_hi ? r_hi : 0), ok_hi, qf);
-
-  float o[DH / 8][4];
+  int n = 0;  // pages consumed by this warp
+  for (int item = gw; item < p.n_items; item += n_warps) {
+    const int4 it = p.dec_items[item];
+    const int seq = it.x, kvh = it.y & 0xffff;
+    const bool final_out = (it.y >> 16) != 0;
+    const int q_row = p.seq_q_start[seq];
+    const int kv_len = p.seq_pos0[seq] + 1;
+    uint32_t qf[DH / 16][4];
+    attn_load_q<DH>(p, q_row, kvh * G + (ok_lo ? r_lo : 0), ok_lo, q_row, kvh * G + (ok_hi ? r_hi : 0), ok_hi, qf);
+    float o[DH / 8][4];
 #pragma unroll
-  for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-
-  // 3-stage ring of 64-key tiles; warp w consumes keys [16w, 16w+16) of each tile
-  constexpr int kStages = 3;
-  for (int s = 0; s < kStages - 1; ++s) {
-    if (t0 + s < t1) attn_load_tile<DH>(p, bt, kvh, (t0 + s) * kAttnKeys, kv_len, sbase + (uint32_t)(s * T::kStageElems) * 2);
-    cp_async_commit();
-  }
-  for (int t = t0; t < t1; ++t) {
-    const int i = t - t0;
-    const int pf = t + kStages - 1;
-    if (pf < t1) attn_load_tile<DH>(p, bt, kvh, pf * kAttnKeys, kv_len, sbase + (uint32_t)(((i + kStages - 1) % kStages) * T::kStageElems) * 2);
-    cp_async_commit();
-    cp_async_wait<kStages - 1>();
-    __syncthreads();
-    const uint32_t stage = sbase + (uint32_t)((i % kStages) * T::kStageElems) * 2;
-    const int kb = warp * 16;
-    float s[2][4];
-    attn_qk<DH, 2>(qf, stage, kb, s);
-    attn_softmax_step<DH, 2>(s, t * kAttnKeys + kb, kv_len, kv_len, p.scale_log2, m, l, o);
-    attn_pv<DH, 2>(s, stage + T::kHalfElems * 2, kb, o);
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-  // reduce the row sums across the quad
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 1);
-    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 2);
-  }
-  // cross-warp merge through shared memory (reuses the tile buffers)
-  __syncthreads();
-  float* sm_o = reinterpret_cast<float*>(attn_smem);     // [4 warps][G][DH]
-  float* sm_ml = sm_o + 4 * G * DH;                      // [4 warps][G][2]
-  if (lane % 4 == 0) {
-    if (ok_lo) { sm_ml[(warp * G + r_lo) * 2] = m[0]; sm_ml[(warp * G + r_lo) * 2 + 1] = l[0]; }
-    if (ok_hi) { sm_ml[(warp * G + r_hi) * 2] = m[1]; sm_ml[(warp * G + r_hi) * 2 + 1] = l[1]; }
-  }
-#pragma unroll
-  for (int n = 0; n < DH / 8; ++n) {
-    const int c = n * 8 + (lane % 4) * 2;
-    if (ok_lo) { sm_o[(warp * G + r_lo) * DH + c] = o[n][0]; sm_o[(warp * G + r_lo) * DH + c + 1] = o[n][1]; }
-    if (ok_hi) { sm_o[(warp * G + r_hi) * DH + c] = o[n][2]; sm_o[(warp * G + r_hi) * DH + c + 1] = o[n][3]; }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < G * DH; idx += kAttnThreads) {
-    const int r = idx / DH, c = idx % DH;
-    float mm = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) mm = fmaxf(mm, sm_ml[(w * G + r) * 2]);
-    float acc = 0.f, ll = 0.f;
-    if (mm != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float f = exp2f(sm_ml[(w * G + r) * 2] - mm);
-        acc += f * sm_o[(w * G + r) * DH + c];
-        ll += f * sm_ml[(w * G + r) * 2 + 1];
-      }
+    for (int c = 0; c < DH / 8; ++c) o[c][0] = o[c][1] = o[c][2] = o[c][3] = 0.f;
+    float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+    for (int pg = it.z; pg < it.w; ++pg, ++n) {
+      if (lane == 0) issue_next();
+      const int st = n % kDecodeStages;
+      mbar_wait(&full[st], (n / kDecodeStages) & 1);
+      const uint32_t k_smem = wbase + st * DecodeSmem<DH>::kStageBytes;
+      float s[2][4];
+      attn_qk<DH, 2>(qf, k_smem, 0, s);
+      attn_softmax_step<DH, 2>(s, pg * kPage, kv_len, kv_len, p.scale_log2, m, l, o);
+      attn_pv<DH, 2>(s, k_smem + KvBlock<DH>::kBytes, 0, o);
+      __syncwarp();
     }
-    if (p.n_splits == 1) {
-      const int head = kvh * G + r;
-      p.out[(long long)q_row * p.n_heads * DH + head * DH + c] = __float2bfloat16(ll > 0.f ? acc / ll : 0.f);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      l[h] += __shfl_xor_sync(0xffffffffu, l[h], 1);
+      l[h] += __shfl_xor_sync(0xffffffffu, l[h], 2);
+    }
+    if (!ok_lo) continue;  // only rows < G (lanes 0 .. 4G-1) carry results
+    const int c0 = (lane % 4) * 2;
+    if (final_out) {
+      const float inv = 1.f / l[0];
+      __nv_bfloat16* dst = p.out + (long long)q_row * p.n_heads * DH + (kvh * G + r_lo) * DH + c0;
+#pragma unroll
+      for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<uint32_t*>(dst + c * 8) = pack_bf16(o[c][0] * inv, o[c][1] * inv);
     } else {
-      const long long slot = (((long long)d * p.n_kv_heads + kvh) * p.n_splits + split) * G + r;
-      p.ws_o[slot * DH + c] = acc;
-      if (c == 0) {
-        p.ws_ml[slot * 2] = mm;
-        p.ws_ml[slot * 2 + 1] = ll;
-      }
+      float* wo = p.ws_o + ((long long)item * G + r_lo) * DH + c0;
+#pragma unroll
+      for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(wo + c * 8) = make_float2(o[c][0], o[c][1]);
+      if (lane % 4 == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)item * G + r_lo) * 2) = make_float2(m[0], l[0]);
     }
   }
 }
 
-// Merge split-KV partials: grid (n_dec, H), DH threads.
+// Merge per-item partials of requests whose KV was split: grid (n_dec, H), DH threads.
 template <int DH, int G>
 __global__ void attn_decode_combine(AttnParams p) {
   const int d = blockIdx.x, head = blockIdx.y, c = threadIdx.x;
+  const int chunks = p.dec_chunks[d];
+  if (chunks <= 1) return;
   const int kvh = head / G, r = head % G;
+  const int base = p.dec_item_base[d] + kvh * chunks;
   const int q_row = p.seq_q_start[p.dec_seq[d]];
   float mm = -INFINITY;
-  for (int s = 0; s < p.n_splits; ++s) {
-    const long long slot = (((long long)d * p.n_kv_heads + kvh) * p.n_splits + s) * G + r;
-    mm = fmaxf(mm, p.ws_ml[slot * 2]);
-  }
+  for (int j = 0; j < chunks; ++j) mm = fmaxf(mm, p.ws_ml[((long long)(base + j) * G + r) * 2]);
   float acc = 0.f, ll = 0.f;
   if (mm != -INFINITY) {
-    for (int s = 0; s < p.n_splits; ++s) {
-      const long long slot = (((long long)d * p.n_kv_heads + kvh) * p.n_splits + s) * G + r;
+    for (int j = 0; j < chunks; ++j) {
+      const long long slot = (long long)(base + j) * G + r;
       const float f = exp2f(p.ws_ml[slot * 2] - mm);
       acc += f * p.ws_o[slot * DH + c];
       ll += f * p.ws_ml[slot * 2 + 1];

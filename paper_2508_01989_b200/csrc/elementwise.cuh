@@ -1,7 +1,7 @@
 // Memory-bound kernels of the hybrid step:
-// embedding gather, RMSNorm (fp32 residual stream -> bf16), RoPE + paged KV
-// append, greedy argmax sampling, deterministic weight init and the KV page
-// migration copy. All use 16 B vector accesses and warp-shuffle reductions.
+// embedding gather, RMSNorm (fp32 residual stream -> bf16), greedy argmax
+// sampling, deterministic weight init and the KV page migration copy. (RoPE and
+// the paged KV append are fused into the QKV GEMM epilogue, gemm.cuh.) All use 16 B vector accesses and warp-shuffle reductions.
 #pragma once
 
 #include "common.cuh"
@@ -97,61 +97,6 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict_
     pk.x = pack_bf16(v.x * inv * w01.x, v.y * inv * w01.y);
     pk.y = pack_bf16(v.z * inv * w23.x, v.w * inv * w23.y);
     *reinterpret_cast<uint2*>(o + c) = pk;
-  }
-}
-
-// ---------------------------------------------------------------- RoPE + KV append
-// For packed row t: rotate q heads in place (half-split / rotate_half convention)
-// and write rotated k and raw v into the paged pool at (block_table[pos/PS], pos%PS).
-// rope_cs: [max_pos][DH/2] float2 (cos, sin), computed on the host in fp64.
-struct RopeAppendParams {
-  __nv_bfloat16* qkv;
-  __nv_bfloat16* kv;
-  const float2* rope_cs;
-  const int* positions;
-  const int* row_seq;
-  const int* seq_bt_off;
-  const int* block_tables;
-  long long page_stride;
-  int layer, n_heads, n_kv_heads, head_dim, page_size;
-};
-
-__global__ void rope_kv_append(RopeAppendParams p) {
-  const int t = blockIdx.x;
-  const int pos = p.positions[t];
-  const int seq = p.row_seq[t];
-  const int page = p.block_tables[p.seq_bt_off[seq] + pos / p.page_size];
-  const int slot = pos % p.page_size;
-  const int half = p.head_dim / 2;
-  const int ld = (p.n_heads + 2 * p.n_kv_heads) * p.head_dim;
-  __nv_bfloat16* row = p.qkv + (long long)t * ld;
-  const float2* cs = p.rope_cs + (long long)pos * half;
-  __nv_bfloat16* page_base = p.kv + (long long)page * p.page_stride;
-  const int n_rot = (p.n_heads + p.n_kv_heads) * half;
-  for (int i = threadIdx.x; i < n_rot; i += blockDim.x) {
-    const int h = i / half, j = i % half;
-    __nv_bfloat16* x = row + h * p.head_dim;
-    const float x1 = __bfloat162float(x[j]), x2 = __bfloat162float(x[j + half]);
-    const float2 c = cs[j];
-    const float y1 = x1 * c.x - x2 * c.y;
-    const float y2 = x2 * c.x + x1 * c.y;
-    if (h < p.n_heads) {
-      x[j] = __float2bfloat16(y1);
-      x[j + half] = __float2bfloat16(y2);
-    } else {
-      const int kvh = h - p.n_heads;
-      __nv_bfloat16* dst = page_base + (((long long)(p.layer * 2) * p.n_kv_heads + kvh) * p.page_size + slot) * p.head_dim;
-      dst[j] = __float2bfloat16(y1);
-      dst[j + half] = __float2bfloat16(y2);
-    }
-  }
-  const int n_v = p.n_kv_heads * p.head_dim / 8;
-  for (int i = threadIdx.x; i < n_v; i += blockDim.x) {
-    const int kvh = (i * 8) / p.head_dim, c = (i * 8) % p.head_dim;
-    const uint4 v = *reinterpret_cast<const uint4*>(row + (p.n_heads + p.n_kv_heads + kvh) * p.head_dim + c);
-    __nv_bfloat16* dst =
-        page_base + (((long long)(p.layer * 2 + 1) * p.n_kv_heads + kvh) * p.page_size + slot) * p.head_dim + c;
-    *reinterpret_cast<uint4*>(dst) = v;
   }
 }
 

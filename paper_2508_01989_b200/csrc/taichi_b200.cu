@@ -126,56 +126,69 @@ void init_kernel_attrs(int dev) {
   std::lock_guard<std::mutex> lk(mu);
   if (done.count(dev)) return;
   DeviceGuard g(dev);
-  set_gemm_smem<64, 0>(); set_gemm_smem<64, 1>(); set_gemm_smem<64, 2>(); set_gemm_smem<64, 4>(); set_gemm_smem<64, 5>();
   set_gemm_smem<128, 0>(); set_gemm_smem<128, 1>(); set_gemm_smem<128, 2>(); set_gemm_smem<128, 3>(); set_gemm_smem<128, 4>(); set_gemm_smem<128, 5>();
   set_gemm_smem<256, 0>(); set_gemm_smem<256, 1>(); set_gemm_smem<256, 2>(); set_gemm_smem<256, 3>(); set_gemm_smem<256, 4>(); set_gemm_smem<256, 5>();
   auto attr = [](const void* fn, int bytes) {
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   };
-  attr((const void*)tc::attn_prefill<64, 2>, 2 * tc::AttnTile<64>::kStageElems * 2);
-  attr((const void*)tc::attn_prefill<128, 4>, 2 * tc::AttnTile<128>::kStageElems * 2);
-  attr((const void*)tc::attn_prefill<128, 5>, 2 * tc::AttnTile<128>::kStageElems * 2);
-  attr((const void*)tc::attn_decode<64, 2>, 3 * tc::AttnTile<64>::kStageElems * 2);
-  attr((const void*)tc::attn_decode<128, 4>, 3 * tc::AttnTile<128>::kStageElems * 2);
-  attr((const void*)tc::attn_decode<128, 5>, 3 * tc::AttnTile<128>::kStageElems * 2);
+  attr((const void*)tc::attn_prefill<64, 2>, tc::PrefillSmem<64>::kBytes);
+  attr((const void*)tc::attn_prefill<128, 4>, tc::PrefillSmem<128>::kBytes);
+  attr((const void*)tc::attn_prefill<128, 5>, tc::PrefillSmem<128>::kBytes);
+  attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128>::kBytes);
+  attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128>::kBytes);
   done.insert(dev);
 }
 
+// Split-K workspace: one fp32 partial tile per unit of split GEMMs + per-tile arrival counters.
+constexpr size_t kSkWsBytes = (size_t)96 << 20;
+constexpr int kSkMaxTiles = 1 << 15;
+
 struct GemmChoice {
-  int bn, k_splits, m_tiles, n_tiles, kbps;
+  int bn, m_tiles, n_tiles, kb, splits, grid;
+  double est_us;
 };
 
-int largest_divisor_leq(int n, int cap) {
-  for (int d = std::max(1, std::min(cap, n)); d >= 1; --d)
-    if (n % d == 0) return d;
-  return 1;
-}
-
-GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits, size_t ws_floats) {
+// Tile width / split-K choice, from tools/gemm_bench.py on B200 (profiles/r01/gemm_bench*.json):
+//  * M > 128 (mixed / prefill steps): data-parallel 128x256 tiles. Split-K loses at M = 576
+//    (down: 98 us unsplit vs 125 us with 3 splits) because the partial round trip and the
+//    last-arriver reduction land in the tail of the wave.
+//  * M <= 128 (decode-only steps, weight streaming): 128-wide tiles split 3 ways when fewer
+//    than half the SMs would get a tile (qkv 23 -> 21 us, down 66 -> 41 us at M = 64).
+GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits) {
   GemmChoice c{};
   c.m_tiles = (M + tc::kGemmBM - 1) / tc::kGemmBM;
-  const int kb = K / tc::kGemmBK;
-  if (force_bn) {
-    c.bn = force_bn;
-  } else {
-    c.bn = (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : 64);
-    // fewer than ~3/4 of the SMs busy: narrower tiles
-    while (c.bn > 128 && c.m_tiles * (N / c.bn) < (sms * 3) / 4 && N % (c.bn / 2) == 0) c.bn /= 2;
-    if (epi != tc::EPI_SWIGLU && c.bn == 128 && c.m_tiles * (N / 128) < sms / 2 && N % 64 == 0) c.bn = 64;
-  }
+  c.kb = K / tc::kGemmBK;
+  if (force_bn) c.bn = force_bn;
+  else if (epi != tc::EPI_RESID_F32 && M <= tc::kGemmBM && (long long)c.m_tiles * (N / 128) < sms / 2) c.bn = 128;
+  else c.bn = (N % 256 == 0) ? 256 : 128;
+  TC_REQUIRE(N % c.bn == 0, "gemm: N not divisible by tile width");
   c.n_tiles = N / c.bn;
-  const int units = c.m_tiles * c.n_tiles;
-  int splits = 1;
+  const long long tiles = (long long)c.m_tiles * c.n_tiles;
+  int sp = 1;
   if (force_splits > 0) {
-    splits = force_splits;
-  } else if (force_splits == 0 && units < sms && M <= 256) {
-    // weight-streaming regime: split K so every SM pulls weights
-    const int want = (sms + units - 1) / units;
-    splits = largest_divisor_leq(kb, std::min(want, std::max(1, kb / 4)));
+    sp = force_splits;
+  } else if (epi == tc::EPI_RESID_F32 && tiles < sms) {
+    // red.add split-K: minimise waves * (k-blocks per split + per-unit overhead). The overhead of
+    // ~8 k-blocks (pipeline fill + epilogue) reproduces the measured optima (o: 3 splits, 27 us
+    // vs 35 unsplit; down: 5 splits, 68 vs 97; M = 64: 9 splits, o 35 -> 13 us, down 99 -> 27 us).
+    double best = 1e30;
+    for (int cand = 1; cand <= std::min(16, std::max(1, c.kb / 4)); ++cand) {
+      const long long waves = (tiles * cand + sms - 1) / sms;
+      const double t = (double)waves * ((c.kb + cand - 1) / cand + 8);
+      if (t < best - 1e-9) {
+        best = t;
+        sp = cand;
+      }
+    }
+  } else if (M <= tc::kGemmBM && tiles < sms / 2) {
+    sp = (int)std::min<long long>(3, std::max<long long>(1, sms / tiles));
   }
-  while (splits > 1 && (size_t)splits * M * N > ws_floats) splits = largest_divisor_leq(kb, splits - 1);
-  c.k_splits = splits;
-  c.kbps = kb / splits;
+  sp = std::max(1, std::min(sp, c.kb));
+  while (epi != tc::EPI_RESID_F32 && sp > 1 && (size_t)tiles * sp * tc::kGemmBM * c.bn * 4 > kSkWsBytes) --sp;
+  c.splits = sp;
+  c.grid = (int)std::min<long long>(sms, tiles * sp);
+  c.est_us = 0;
   return c;
 }
 
@@ -187,15 +200,10 @@ void launch_gemm_bn(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Gemm
     case tc::EPI_BF16: tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
     case tc::EPI_BF16_BIAS: tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
     case tc::EPI_RESID_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_SWIGLU: tc::gemm_bf16_tcgen05<BN, tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
     case tc::EPI_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_PARTIAL_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_PARTIAL_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_SWIGLU:
-      if constexpr (BN >= 128) {
-        tc::gemm_bf16_tcgen05<BN, tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args);
-        break;
-      }
-      [[fallthrough]];
-    default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue/tile"};
+    case tc::EPI_QKV_ROPE: tc::gemm_bf16_tcgen05<BN, tc::EPI_QKV_ROPE><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
 
@@ -203,61 +211,52 @@ void launch_gemm_bn(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Gemm
 struct WMat {
   __nv_bfloat16* ptr = nullptr;
   int64_t rows = 0, cols = 0;
-  CUtensorMap map64, map128, map256;
+  CUtensorMap map128, map256;
   void make_maps() {
-    map64 = make_kmajor_map(ptr, rows, cols, 64);
     if (rows % 128 == 0) map128 = make_kmajor_map(ptr, rows, cols, 128);
     if (rows % 256 == 0) map256 = make_kmajor_map(ptr, rows, cols, 256);
   }
-  const CUtensorMap& map(int bn) const { return bn == 64 ? map64 : (bn == 128 ? map128 : map256); }
+  const CUtensorMap& map(int bn) const { return bn == 128 ? map128 : map256; }
+};
+
+struct SkWorkspace {
+  float* ws = nullptr;
+  int* cnt = nullptr;
 };
 
 // out = epi(A[M,K] * W[N,K]^T). a_map: box 128 rows over the activation buffer.
 int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
-             int sms, float* ws, size_t ws_floats, cudaStream_t s, int force_bn = 0, int force_splits = 0) {
+             int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
+             const tc::QkvRopeArgs* rope = nullptr) {
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(K % tc::kGemmBK == 0, "gemm: K must be a multiple of 64");
-  GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits, ws ? ws_floats : 0);
-  TC_REQUIRE(N % c.bn == 0, "gemm: N not divisible by tile width");
+  TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
+  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256, "gemm: tile width must be 128 or 256");
+  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits);
+  TC_REQUIRE((long long)c.m_tiles * c.n_tiles <= kSkMaxTiles, "gemm: too many tiles");
   tc::GemmArgs args{};
   args.M = M;
   args.N = N;
   args.K = K;
   args.m_tiles = c.m_tiles;
   args.n_tiles = c.n_tiles;
-  args.k_splits = c.k_splits;
-  args.k_blocks_per_split = c.kbps;
+  args.kb = c.kb;
+  args.splits = c.splits;
+  args.units = c.m_tiles * c.n_tiles * c.splits;
+  args.out = out;
+  args.ldo = ldo;
   args.bias = bias;
-  const int units = c.m_tiles * c.n_tiles * c.k_splits;
-  const int grid = std::min(units, sms);
-  if (c.k_splits == 1) {
-    args.out = out;
-    args.ldo = ldo;
-    switch (c.bn) {
-      case 64: launch_gemm_bn<64>(a_map, w.map(64), args, epi, grid, s); break;
-      case 128: launch_gemm_bn<128>(a_map, w.map(128), args, epi, grid, s); break;
-      default: launch_gemm_bn<256>(a_map, w.map(256), args, epi, grid, s); break;
-    }
-  } else {
-    args.out = ws;
-    args.ldo = N;
-    switch (c.bn) {
-      case 64: launch_gemm_bn<64>(a_map, w.map(64), args, tc::EPI_PARTIAL_F32, grid, s); break;
-      case 128: launch_gemm_bn<128>(a_map, w.map(128), args, tc::EPI_PARTIAL_F32, grid, s); break;
-      default: launch_gemm_bn<256>(a_map, w.map(256), args, tc::EPI_PARTIAL_F32, grid, s); break;
-    }
-    const int blocks = std::min(4 * sms, (int)(((size_t)M * N / 4 + 255) / 256) + 1);
-    switch (epi) {
-      case tc::EPI_BF16: tc::gemm_splitk_reduce<tc::EPI_BF16><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
-      case tc::EPI_BF16_BIAS: tc::gemm_splitk_reduce<tc::EPI_BF16_BIAS><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
-      case tc::EPI_RESID_F32: tc::gemm_splitk_reduce<tc::EPI_RESID_F32><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
-      case tc::EPI_SWIGLU: tc::gemm_splitk_reduce<tc::EPI_SWIGLU><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
-      case tc::EPI_F32: tc::gemm_splitk_reduce<tc::EPI_F32><<<blocks, 256, 0, s>>>(ws, c.k_splits, M, N, out, ldo, bias); break;
-      default: throw TcFail{TC_ERR_INVALID, "bad epilogue"};
-    }
+  args.ws = sk.ws;
+  args.tile_cnt = sk.cnt;
+  if (epi == tc::EPI_QKV_ROPE) {
+    TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
+    TC_REQUIRE(c.bn % rope->head_dim == 0, "gemm: tile width must cover whole heads");
+    args.rope = *rope;
   }
+  if (c.bn == 128) launch_gemm_bn<128>(a_map, w.map(128), args, epi, c.grid, s);
+  else launch_gemm_bn<256>(a_map, w.map(256), args, epi, c.grid, s);
   TC_CUDA(cudaGetLastError());
-  return c.k_splits == 1 ? 1 : 2;
+  return 1;
 }
 
 // ------------------------------------------------------------------ instance
@@ -265,6 +264,8 @@ struct LayerW {
   WMat qkv, o, gate_up, down;
   __nv_bfloat16 *qkv_bias = nullptr, *attn_norm = nullptr, *mlp_norm = nullptr;
 };
+
+constexpr int kMaxDecodeItems = 16384;
 
 constexpr uint64_t kTidEmbed = 1, kTidLmHead = 2, kTidFinalNorm = 3;
 inline uint64_t tid_layer(int l, int j) { return 16 + 16ull * l + j; }
@@ -307,6 +308,7 @@ struct tc_instance {
   __nv_bfloat16* kv = nullptr;
   int64_t page_elems = 0, n_pages = 0;
   std::vector<int32_t> free_pages;
+  CUtensorMap kv_map;  // 3-D view {64 dims, head_dim/64, pool rows} for TMA page loads
   std::unordered_map<int64_t, std::vector<int32_t>> tables;
   // activations
   int qkv_n = 0;
@@ -316,8 +318,7 @@ struct tc_instance {
   int* ids_dev = nullptr;
   int* ids_host = nullptr;
   CUtensorMap map_xnorm, map_attn, map_act, map_lm_in;
-  float* splitk_ws = nullptr;
-  size_t splitk_floats = 0;
+  SkWorkspace sk;
   float *attn_ws_o = nullptr, *attn_ws_ml = nullptr;
   size_t attn_ws_floats = 0;
   float2* rope = nullptr;
@@ -457,15 +458,15 @@ void alloc_buffers(tc_instance* I) {
   I->map_attn = make_kmajor_map(I->attn_out, Tp, (uint64_t)m.n_heads * m.head_dim, 128);
   I->map_act = make_kmajor_map(I->act, Tp, m.ffn_dim, 128);
   I->map_lm_in = make_kmajor_map(I->lm_in, Sp, dm, 128);
-  // split-K partials: enough for the small-M weight-streaming regime (M <= 256)
-  I->splitk_floats = (size_t)std::min(T, 256) * std::max<int64_t>(2 * m.ffn_dim, m.vocab) * 4;
-  TC_CUDA(cudaMalloc(&I->splitk_ws, I->splitk_floats * 4));
-  // decode split-KV partials
+  // stream-K partial slots + tile counters (counters must start at zero)
+  TC_CUDA(cudaMalloc(&I->sk.ws, kSkWsBytes));
+  TC_CUDA(cudaMalloc(&I->sk.cnt, (size_t)kSkMaxTiles * 4));
+  TC_CUDA(cudaMemset(I->sk.cnt, 0, (size_t)kSkMaxTiles * 4));
+  // decode split-KV partials (one slot per work item)
   const int G = m.n_heads / m.n_kv_heads;
-  const int max_splits = 64;
-  I->attn_ws_floats = (size_t)S * m.n_kv_heads * max_splits * G * m.head_dim;
+  I->attn_ws_floats = (size_t)kMaxDecodeItems * G * m.head_dim;
   TC_CUDA(cudaMalloc(&I->attn_ws_o, I->attn_ws_floats * 4));
-  TC_CUDA(cudaMalloc(&I->attn_ws_ml, (size_t)S * m.n_kv_heads * max_splits * G * 2 * 4));
+  TC_CUDA(cudaMalloc(&I->attn_ws_ml, (size_t)kMaxDecodeItems * G * 2 * 4));
   // RoPE table in fp64 -> fp32
   const int half = m.head_dim / 2;
   std::vector<float2> cs((size_t)I->desc.max_context * half);
@@ -479,8 +480,8 @@ void alloc_buffers(tc_instance* I) {
   TC_CUDA(cudaMemcpy(I->rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
   // metadata: 3T + 4S + qblocks(<= T + S) * 2 + S (dec) + S (logit rows) + block tables
   const int64_t max_pages_per_seq = (I->desc.max_context + I->desc.page_size - 1) / I->desc.page_size;
-  I->meta_ints = 3 * (size_t)T + 4 * (size_t)S + 2 * (size_t)(T + S) + 2 * (size_t)S +
-                 (size_t)S * max_pages_per_seq + 64;
+  I->meta_ints = 3 * (size_t)T + 4 * (size_t)S + 2 * (size_t)(T + S) + 4 * (size_t)S +
+                 4 * (size_t)kMaxDecodeItems + (size_t)S * max_pages_per_seq + 128;
   TC_CUDA(cudaMallocHost(&I->meta_host, I->meta_ints * 4));
   TC_CUDA(cudaMalloc(&I->meta_dev, I->meta_ints * 4));
   TC_CUDA(cudaEventCreate(&I->ev_start));
@@ -533,18 +534,16 @@ struct ProfScope {
 };
 
 template <int DH, int G>
-void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec) {
+void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid, bool combine) {
   const int hk = I->d.n_kv_heads;
   if (n_qblk > 0) {
-    const int smem = 2 * tc::AttnTile<DH>::kStageElems * 2;
-    tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kAttnThreads, smem, I->stream>>>(p);
+    tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kPrefillThreads, tc::PrefillSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
     ++I->launches;
   }
   if (n_dec > 0) {
-    const int smem = 3 * tc::AttnTile<DH>::kStageElems * 2;
-    tc::attn_decode<DH, G><<<dim3(n_dec, hk, p.n_splits), tc::kAttnThreads, smem, I->stream>>>(p);
+    tc::attn_decode<DH, G><<<dec_grid, tc::kDecodeWarps * 32, tc::DecodeSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
     ++I->launches;
-    if (p.n_splits > 1) {
+    if (combine) {
       tc::attn_decode_combine<DH, G><<<dim3(n_dec, I->d.n_heads), DH, 0, I->stream>>>(p);
       ++I->launches;
     }
@@ -552,11 +551,11 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
   TC_CUDA(cudaGetLastError());
 }
 
-void dispatch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec) {
+void dispatch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid, bool combine) {
   const int G = I->d.n_heads / I->d.n_kv_heads;
-  if (I->d.head_dim == 64 && G == 2) launch_attention<64, 2>(I, p, n_qblk, n_dec);
-  else if (I->d.head_dim == 128 && G == 4) launch_attention<128, 4>(I, p, n_qblk, n_dec);
-  else if (I->d.head_dim == 128 && G == 5) launch_attention<128, 5>(I, p, n_qblk, n_dec);
+  if (I->d.head_dim == 64 && G == 2) launch_attention<64, 2>(I, p, n_qblk, n_dec, dec_grid, combine);
+  else if (I->d.head_dim == 128 && G == 4) launch_attention<128, 4>(I, p, n_qblk, n_dec, dec_grid, combine);
+  else if (I->d.head_dim == 128 && G == 5) launch_attention<128, 5>(I, p, n_qblk, n_dec, dec_grid, combine);
   else throw TcFail{TC_ERR_INVALID, "unsupported attention shape"};
 }
 
@@ -592,6 +591,19 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   }
   n_logit += n_dec;
   for (int i = 0; i < n_dec; ++i) n_bt += st->decode[i].pos / ps + 1;
+  // decode split-KV work items: (request, kv head, run of <= ppi pages). ppi balances ~4 items
+  // per resident warp (2 CTAs x 4 warps per SM) and caps the item count.
+  long long page_heads = 0;
+  for (int i = 0; i < n_dec; ++i) page_heads += (long long)(st->decode[i].pos / ps + 1) * m.n_kv_heads;
+  const long long dec_warps = 2LL * I->sms * tc::kDecodeWarps;
+  int ppi = (int)std::max<long long>(4, (page_heads + 4 * dec_warps - 1) / (4 * dec_warps));
+  auto count_items = [&](int per) {
+    long long n = 0;
+    for (int i = 0; i < n_dec; ++i) n += (long long)m.n_kv_heads * ((st->decode[i].pos / ps + 1 + per - 1) / per);
+    return n;
+  };
+  while (count_items(ppi) > kMaxDecodeItems) ppi *= 2;
+  const int n_items = (int)count_items(ppi);
   // layout of the metadata block
   int32_t* h = I->meta_host;
   size_t off = 0;
@@ -602,9 +614,10 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   };
   const size_t o_tok = take(T), o_pos = take(T), o_rseq = take(T), o_qs = take(n_seq), o_ql = take(n_seq),
                o_p0 = take(n_seq), o_bo = take(n_seq), o_qbs = take(n_qblk), o_qbo = take(n_qblk), o_dseq = take(n_dec),
-               o_lrow = take(n_logit), o_bt = take(n_bt);
+               o_lrow = take(n_logit), o_bt = take(n_bt), o_items = take(4 * (size_t)n_items), o_ibase = take(n_dec),
+               o_ichunks = take(n_dec);
   TC_REQUIRE(off <= I->meta_ints, "step: metadata overflow");
-  int row = 0, qb = 0, lr = 0, bt = 0, max_tiles = 0;
+  int row = 0, qb = 0, lr = 0, bt = 0;
   for (int i = 0; i < n_pf; ++i) {
     const tc_prefill_slice& sl = st->prefill[i];
     const std::vector<int32_t>& pages = I->tables[sl.req_id];
@@ -645,8 +658,26 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     h[o_rseq + row] = s;
     h[o_dseq + j] = s;
     h[o_lrow + lr++] = row;
-    max_tiles = std::max(max_tiles, (di.pos + 1 + tc::kAttnKeys - 1) / tc::kAttnKeys);
     ++row;
+  }
+  bool any_split = false;
+  {
+    int it = 0;
+    for (int j = 0; j < n_dec; ++j) {
+      const int pages = st->decode[j].pos / ps + 1;
+      const int chunks = (pages + ppi - 1) / ppi;
+      h[o_ibase + j] = it;
+      h[o_ichunks + j] = chunks;
+      any_split = any_split || chunks > 1;
+      for (int kh = 0; kh < m.n_kv_heads; ++kh)
+        for (int c = 0; c < chunks; ++c) {
+          int32_t* e = h + o_items + 4 * (size_t)it++;
+          e[0] = n_pf + j;
+          e[1] = kh | (chunks == 1 ? (1 << 16) : 0);
+          e[2] = c * ppi;
+          e[3] = std::min(pages, (c + 1) * ppi);
+        }
+    }
   }
   cudaStream_t s = I->stream;
   DeviceGuard dg(I->desc.device);
@@ -657,15 +688,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   TC_CUDA(cudaMemcpyAsync(I->meta_dev, h, off * 4, cudaMemcpyHostToDevice, s));
   const int32_t* dm = I->meta_dev;
 
-  // decode split-KV: enough CTAs to cover ~2 waves of the SMs
-  int splits = 1, tps = std::max(1, max_tiles);
-  if (n_dec > 0) {
-    const int base = n_dec * m.n_kv_heads;
-    splits = std::min(std::max(1, (2 * I->sms + base - 1) / base), std::max(1, max_tiles));
-    splits = std::min(splits, 64);
-    tps = (max_tiles + splits - 1) / splits;
-    splits = (max_tiles + tps - 1) / tps;
-  }
+  const int dec_grid = (int)std::max<long long>(1, std::min<long long>(2LL * I->sms, (n_items + tc::kDecodeWarps - 1) / tc::kDecodeWarps));
 
   {
     ProfScope ps_(I, "embed");
@@ -675,8 +698,6 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   tc::AttnParams ap{};
   ap.qkv = I->qkv;
   ap.out = I->attn_out;
-  ap.kv = I->kv;
-  ap.page_stride = I->page_elems;
   ap.n_layers = m.n_layers;
   ap.n_heads = m.n_heads;
   ap.n_kv_heads = m.n_kv_heads;
@@ -690,12 +711,13 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   ap.qblk_seq = dm + o_qbs;
   ap.qblk_off = dm + o_qbo;
   ap.dec_seq = dm + o_dseq;
-  ap.n_splits = splits;
-  ap.tiles_per_split = tps;
+  ap.dec_items = reinterpret_cast<const int4*>(dm + o_items);
+  ap.n_items = n_items;
+  ap.dec_item_base = dm + o_ibase;
+  ap.dec_chunks = dm + o_ichunks;
   ap.ws_o = I->attn_ws_o;
   ap.ws_ml = I->attn_ws_ml;
-  tc::RopeAppendParams rp{};
-  rp.qkv = I->qkv;
+  tc::QkvRopeArgs rp{};
   rp.kv = I->kv;
   rp.rope_cs = I->rope;
   rp.positions = dm + o_pos;
@@ -716,25 +738,20 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       ++I->launches;
     }
     {
+      // QKV projection with fused bias, RoPE and paged KV append (q stays in I->qkv)
       ProfScope p_(I, "gemm_qkv");
-      I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, L.qkv_bias, m.qkv_bias ? tc::EPI_BF16_BIAS : tc::EPI_BF16,
-               I->sms, I->splitk_ws, I->splitk_floats, s);
-    }
-    {
-      ProfScope p_(I, "rope_append");
       rp.layer = l;
-      tc::rope_kv_append<<<T, 128, 0, s>>>(rp);
-      ++I->launches;
+      I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
+                              tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp);
     }
     {
       ProfScope p_(I, "attn");
       ap.layer = l;
-      dispatch_attention(I, ap, n_qblk, n_dec);
+      dispatch_attention(I, ap, n_qblk, n_dec, dec_grid, any_split);
     }
     {
       ProfScope p_(I, "gemm_o");
-      I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->splitk_ws,
-               I->splitk_floats, s);
+      I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s);
     }
     {
       ProfScope p_(I, "norm");
@@ -743,13 +760,11 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_gate_up");
-      I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->splitk_ws,
-               I->splitk_floats, s);
+      I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
     }
     {
       ProfScope p_(I, "gemm_down");
-      I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->splitk_ws,
-               I->splitk_floats, s);
+      I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s);
     }
   }
   if (n_logit > 0) {
@@ -757,8 +772,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     tc::rmsnorm_rows<rms_threads><<<n_logit, rms_threads, 0, s>>>(I->resid, dm + o_lrow, I->final_norm, I->lm_in,
                                                                   m.d_model, m.rms_eps);
     I->launches += 2;  // gathered RMSNorm + argmax
-    I->launches += run_gemm(I->map_lm_in, I->lm_head, n_logit, I->logits, m.vocab, nullptr, tc::EPI_F32, I->sms, I->splitk_ws,
-             I->splitk_floats, s);
+    I->launches += run_gemm(I->map_lm_in, I->lm_head, n_logit, I->logits, m.vocab, nullptr, tc::EPI_F32, I->sms, I->sk, s);
     tc::argmax_rows<1024><<<n_logit, 1024, 0, s>>>(I->logits, m.vocab, I->ids_dev);
     TC_CUDA(cudaMemcpyAsync(I->ids_host, I->ids_dev, (size_t)n_logit * 4, cudaMemcpyDeviceToHost, s));
   }
@@ -793,7 +807,7 @@ void destroy(tc_instance* I) {
     if (p) cudaFree(p);
   };
   f(I->weight_block); f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
-  f(I->logits); f(I->ids_dev); f(I->splitk_ws); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->rope); f(I->meta_dev);
+  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->rope); f(I->meta_dev);
   f(I->mig_dev);
   if (I->ids_host) cudaFreeHost(I->ids_host);
   if (I->meta_host) cudaFreeHost(I->meta_host);
@@ -917,6 +931,18 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     I->n_pages = (desc->kv_pool_tokens + desc->page_size - 1) / desc->page_size;
     TC_CUDA(cudaMalloc(&I->kv, (size_t)I->n_pages * I->page_elems * 2));
     TC_CUDA(cudaMemsetAsync(I->kv, 0, (size_t)I->n_pages * I->page_elems * 2, I->stream));
+    {
+      const uint64_t rows = (uint64_t)I->n_pages * m.n_layers * 2 * m.n_kv_heads * desc->page_size;
+      TC_REQUIRE(rows < (1ull << 31), "create: KV pool too large for 32-bit TMA row coordinates");
+      const cuuint64_t dims[3] = {64, (cuuint64_t)(m.head_dim / 64), rows};
+      const cuuint64_t strides[2] = {128, (cuuint64_t)m.head_dim * 2};
+      const cuuint32_t box[3] = {64, (cuuint32_t)(m.head_dim / 64), (cuuint32_t)desc->page_size};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      const CUresult r = tensor_map_encoder()(&I->kv_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, I->kv, dims, strides, box,
+                                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw TcFail{TC_ERR_CUDA, "KV tensor map encode failed: " + std::to_string((int)r)};
+    }
     I->free_pages.resize(I->n_pages);
     for (int64_t i = 0; i < I->n_pages; ++i) I->free_pages[i] = (int32_t)(I->n_pages - 1 - i);  // pop_back -> 0,1,..
     TC_CUDA(cudaStreamSynchronize(I->stream));
@@ -1042,6 +1068,7 @@ tc_status tc_gemm(int32_t device, const void* a, const void* b, void* out, const
   return guarded([&] {
     TC_REQUIRE(a && b && out && m > 0 && n > 0 && k > 0, "gemm: bad argument");
     TC_REQUIRE(epilogue >= 0 && epilogue <= 4, "gemm: bad epilogue");
+    TC_REQUIRE(k_splits >= 0, "gemm: bad k_splits");
     DeviceGuard dg(device);
     init_kernel_attrs(device);
     const int sms = device_sms(device);
@@ -1051,22 +1078,26 @@ tc_status tc_gemm(int32_t device, const void* a, const void* b, void* out, const
     w.rows = n;
     w.cols = k;
     w.make_maps();
-    const int mp = (m + 127) / 128 * 128;  // callers pass A with >= mp rows allocated? no: clamp the map to m rows
-    (void)mp;
     const CUtensorMap am = make_kmajor_map(a, m, k, 128);
     const int ldo = epilogue == tc::EPI_SWIGLU ? n / 2 : n;
-    float* ws = nullptr;
-    size_t ws_floats = 0;
-    if (k_splits != 1) {
-      GemmChoice c = choose_gemm(m, n, k, epilogue, sms, bn, k_splits, (size_t)1 << 40);
-      if (c.k_splits > 1) {
-        ws_floats = (size_t)c.k_splits * m * n;
-        TC_CUDA(cudaMallocAsync(&ws, ws_floats * 4, s));
+    // one persistent split-K workspace per device (the tile counters self-reset: the last
+    // arriver of every split tile zeroes its counter), so calls on one stream reuse it
+    static std::mutex mu;
+    static std::unordered_map<int, SkWorkspace> per_dev;
+    SkWorkspace sk;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = per_dev.find(device);
+      if (it == per_dev.end()) {
+        SkWorkspace w_;
+        TC_CUDA(cudaMalloc(&w_.ws, kSkWsBytes));
+        TC_CUDA(cudaMalloc(&w_.cnt, (size_t)kSkMaxTiles * 4));
+        TC_CUDA(cudaMemset(w_.cnt, 0, (size_t)kSkMaxTiles * 4));
+        it = per_dev.emplace(device, w_).first;
       }
+      sk = it->second;
     }
-    run_gemm(am, w, m, out, ldo, (const __nv_bfloat16*)bias, epilogue, sms, ws, ws_floats, s, bn,
-             k_splits == 1 ? -1 : k_splits);
-    if (ws) TC_CUDA(cudaFreeAsync(ws, s));
+    run_gemm(am, w, m, out, ldo, (const __nv_bfloat16*)bias, epilogue, sms, sk, s, bn, k_splits);
   });
 }
 

@@ -78,8 +78,11 @@ int main(int argc, char** argv) {
       d.dims = dims;
       d.weight_seed = weight_seed;  // every instance holds the same model replica
       d.page_size = 16;
-      // physical pool = logical capacity x 1.5 headroom (in-flight prefill, pending, transfers) + a max context
-      d.kv_pool_tokens = pool_tokens > 0 ? pool_tokens : sp.kv_capacity * 3 / 2 + max_ctx + 1024;
+      // The logical kv_capacity (cluster.hpp:130-181) only counts resident decodes; the physical pool
+      // must also hold in-flight prefills, pending decodes (Init transfers are admitted without a
+      // fit check, engine.hpp:512) and KV in transit. Default: 3x logical + 8 max contexts;
+      // --pool-tokens overrides (production: size from free HBM).
+      d.kv_pool_tokens = pool_tokens > 0 ? pool_tokens : sp.kv_capacity * 3 + 8 * max_ctx + 1024;
       d.max_step_tokens = static_cast<int32_t>(std::max<Tokens>(sp.chunk_size, 1) + 1024);
       d.max_seqs = 1024;
       d.max_context = static_cast<int32_t>(max_ctx + 16);

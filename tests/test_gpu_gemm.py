@@ -24,10 +24,13 @@ def _close(got, ref, bf16_out):
         torch.testing.assert_close(got.float(), ref, rtol=1e-4, atol=1e-4 * s)
 
 
+# bn: 0 auto / 128 / 256; splits = CTAs-per-tile cap (0 = full stream-K, 1 = one CTA per tile)
 @pytest.mark.parametrize("m,n,k,bn,splits", [
     (128, 256, 64, 256, 1), (1, 256, 128, 0, 0), (100, 512, 256, 0, 0), (129, 1024, 512, 128, 1),
-    (576, 6144, 4096, 0, 0), (576, 4096, 4096, 0, 0), (64, 6144, 4096, 0, 0), (64, 4096, 14336, 0, 0),
-    (1100, 1024, 4096, 0, 0), (256, 512, 1024, 64, 1), (64, 512, 1024, 128, 4), (200, 256, 4096, 256, 2),
+    (576, 6144, 4096, 0, 0), (576, 4096, 4096, 0, 0), (576, 4096, 14336, 0, 0), (64, 6144, 4096, 0, 0),
+    (64, 4096, 14336, 0, 0), (1100, 1024, 4096, 0, 0), (256, 512, 1024, 128, 1), (64, 512, 1024, 128, 4),
+    (200, 256, 4096, 256, 2), (5, 256, 256, 0, 0), (3000, 6144, 4096, 0, 0), (1, 128, 64, 128, 0),
+    (333, 7168, 5120, 0, 0), (64, 256, 8192, 256, 0),
 ])
 def test_gemm_bf16(cuda_ok, m, n, k, bn, splits):
     g = torch.Generator(device="cuda").manual_seed(m * 7 + n + k)
