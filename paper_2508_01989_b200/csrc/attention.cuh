@@ -17,8 +17,9 @@
 //  * attn_decode   -- split-KV at warp granularity: a work item is (request,
 //    kv_head, run of pages); a persistent grid of independent warps walks its
 //    items with a private 4-stage page ring (each warp issues its own TMA loads
-//    S-1 pages ahead, across item boundaries). Multi-item requests are merged by
-//    attn_decode_combine.
+//    S-1 pages ahead, across item boundaries). For requests split into several items
+//    the warp that finishes an item LAST (atomic counter per request and kv head)
+//    merges the partials -- no separate combine launch, no waiting.
 #pragma once
 
 #include "common.cuh"
@@ -37,13 +38,14 @@ struct AttnParams {
   const int* block_tables;   // flat page ids
   const int* qblk_seq;       // prefill work list
   const int* qblk_off;
-  const int4* dec_items;     // decode work: (seq, kvh | final << 16, page0, page1)
+  const int4* dec_items;     // decode work: (seq, kvh | decode index << 8, page0, page1)
   int n_items;
   const int* dec_seq;        // decode index -> sequence
   const int* dec_item_base;  // decode index -> first item; items (d, kvh, j) at base + kvh * chunks + j
   const int* dec_chunks;     // decode index -> items per kv head
   float* ws_o;               // [item][G][DH]
   float* ws_ml;              // [item][G][2]
+  int* dec_cnt;              // [decode][kv head] arrival counters (zero; the last arriver resets)
 };
 
 TC_DEVICE void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_co
       if (l_page < 0) l_page = it.z;
       if (l_page < it.w) {
         const int page = p.block_tables[p.seq_bt_off[it.x] + l_page];
-        const int kvh = it.y & 0xffff;
+        const int kvh = it.y & 0xff;
         const int st = issued % kDecodeStages;
         const uint32_t dst = wbase + st * DecodeSmem<DH>::kStageBytes;
         fence_proxy_async();
@@ -367,8 +369,8 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_co
   int n = 0;  // pages consumed by this warp
   for (int item = gw; item < p.n_items; item += n_warps) {
     const int4 it = p.dec_items[item];
-    const int seq = it.x, kvh = it.y & 0xffff;
-    const bool final_out = (it.y >> 16) != 0;
+    const int seq = it.x, kvh = it.y & 0xff, d = it.y >> 8;
+    const int chunks = p.dec_chunks[d];
     const int q_row = p.seq_q_start[seq];
     const int kv_len = p.seq_pos0[seq] + 1;
     uint32_t qf[DH / 16][4];
@@ -393,43 +395,52 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_co
       l[h] += __shfl_xor_sync(0xffffffffu, l[h], 1);
       l[h] += __shfl_xor_sync(0xffffffffu, l[h], 2);
     }
-    if (!ok_lo) continue;  // only rows < G (lanes 0 .. 4G-1) carry results
     const int c0 = (lane % 4) * 2;
-    if (final_out) {
-      const float inv = 1.f / l[0];
-      __nv_bfloat16* dst = p.out + (long long)q_row * p.n_heads * DH + (kvh * G + r_lo) * DH + c0;
+    __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
+    if (chunks == 1) {
+      if (ok_lo) {  // only rows < G (lanes 0 .. 4G-1) carry results
+        const float inv = 1.f / l[0];
 #pragma unroll
-      for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<uint32_t*>(dst + c * 8) = pack_bf16(o[c][0] * inv, o[c][1] * inv);
-    } else {
+        for (int c = 0; c < DH / 8; ++c)
+          *reinterpret_cast<uint32_t*>(out_row + r_lo * DH + c * 8 + c0) = pack_bf16(o[c][0] * inv, o[c][1] * inv);
+      }
+      continue;
+    }
+    if (ok_lo) {
       float* wo = p.ws_o + ((long long)item * G + r_lo) * DH + c0;
 #pragma unroll
       for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(wo + c * 8) = make_float2(o[c][0], o[c][1]);
       if (lane % 4 == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)item * G + r_lo) * 2) = make_float2(m[0], l[0]);
     }
-  }
-}
-
-// Merge per-item partials of requests whose KV was split: grid (n_dec, H), DH threads.
-template <int DH, int G>
-__global__ void attn_decode_combine(AttnParams p) {
-  const int d = blockIdx.x, head = blockIdx.y, c = threadIdx.x;
-  const int chunks = p.dec_chunks[d];
-  if (chunks <= 1) return;
-  const int kvh = head / G, r = head % G;
-  const int base = p.dec_item_base[d] + kvh * chunks;
-  const int q_row = p.seq_q_start[p.dec_seq[d]];
-  float mm = -INFINITY;
-  for (int j = 0; j < chunks; ++j) mm = fmaxf(mm, p.ws_ml[((long long)(base + j) * G + r) * 2]);
-  float acc = 0.f, ll = 0.f;
-  if (mm != -INFINITY) {
-    for (int j = 0; j < chunks; ++j) {
-      const long long slot = (long long)(base + j) * G + r;
-      const float f = exp2f(p.ws_ml[slot * 2] - mm);
-      acc += f * p.ws_o[slot * DH + c];
-      ll += f * p.ws_ml[slot * 2 + 1];
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      int* cnt = p.dec_cnt + d * p.n_kv_heads + kvh;
+      last = atomicAdd(cnt, 1) == chunks - 1;
+      if (last) *cnt = 0;  // ready for the next layer / step
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) continue;
+    __threadfence();
+    // last arriver: merge the request's chunks for this kv head (lane -> DH/32 dims of all G rows)
+    const int base = p.dec_item_base[d] + kvh * chunks;
+    for (int r = 0; r < G; ++r) {
+      float mm = -INFINITY;
+      for (int j = 0; j < chunks; ++j) mm = fmaxf(mm, __ldcg(p.ws_ml + ((long long)(base + j) * G + r) * 2));
+      float acc[DH / 32] = {}, ll = 0.f;
+      for (int j = 0; j < chunks; ++j) {
+        const long long slot = (long long)(base + j) * G + r;
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + slot * 2));
+        const float f = mm == -INFINITY ? 0.f : exp2f(ml.x - mm);
+        ll += f * ml.y;
+#pragma unroll
+        for (int e = 0; e < DH / 32; ++e) acc[e] += f * __ldcg(p.ws_o + slot * DH + e * 32 + lane);
+      }
+      const float inv = ll > 0.f ? 1.f / ll : 0.f;
+#pragma unroll
+      for (int e = 0; e < DH / 32; ++e) out_row[r * DH + e * 32 + lane] = __float2bfloat16(acc[e] * inv);
     }
   }
-  p.out[(long long)q_row * p.n_heads * DH + head * DH + c] = __float2bfloat16(ll > 0.f ? acc / ll : 0.f);
 }
 
 }  // namespace tc

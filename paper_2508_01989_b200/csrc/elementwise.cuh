@@ -65,38 +65,45 @@ __global__ void embed_rows(const int* __restrict__ tokens, const __nv_bfloat16* 
 // ---------------------------------------------------------------- RMSNorm
 // out[r, :] = bf16(x[src_row(r), :] * rsqrt(mean(x^2) + eps) * w), fp32 math.
 // rows == nullptr: identity row map; otherwise gathers rows (sampled-row LM head).
+// The row is read once into registers (<= kMaxVec float4 per thread: d <= 8192).
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict__ x, const int* __restrict__ rows,
                                                         const __nv_bfloat16* __restrict__ w,
                                                         __nv_bfloat16* __restrict__ out, int d, float eps) {
+  constexpr int kMaxVec = 8192 / (4 * THREADS);
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
   const float* xr = x + (long long)src * d;
+  float4 v[kMaxVec];
   float ss = 0.f;
-  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = (i * THREADS + threadIdx.x) * 4;
+    if (c < d) {
+      v[i] = __ldg(reinterpret_cast<const float4*>(xr + c));
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
   }
   __shared__ float red[THREADS / 32];
   ss = warp_sum(ss);
   if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float inv = rsqrtf(red[0] / (float)d + eps);
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < THREADS / 32; ++i) tot += red[i];
+  const float inv = rsqrtf(tot / (float)d + eps);
   __nv_bfloat16* o = out + (long long)r * d;
-  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    const uint2 wb = *reinterpret_cast<const uint2*>(w + c);
-    const float2 w01 = unpack_bf16(wb.x), w23 = unpack_bf16(wb.y);
-    uint2 pk;
-    pk.x = pack_bf16(v.x * inv * w01.x, v.y * inv * w01.y);
-    pk.y = pack_bf16(v.z * inv * w23.x, v.w * inv * w23.y);
-    *reinterpret_cast<uint2*>(o + c) = pk;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = (i * THREADS + threadIdx.x) * 4;
+    if (c < d) {
+      const uint2 wb = __ldg(reinterpret_cast<const uint2*>(w + c));
+      const float2 w01 = unpack_bf16(wb.x), w23 = unpack_bf16(wb.y);
+      uint2 pk;
+      pk.x = pack_bf16(v[i].x * inv * w01.x, v[i].y * inv * w01.y);
+      pk.y = pack_bf16(v[i].z * inv * w23.x, v[i].w * inv * w23.y);
+      *reinterpret_cast<uint2*>(o + c) = pk;
+    }
   }
 }
 

@@ -320,6 +320,7 @@ struct tc_instance {
   CUtensorMap map_xnorm, map_attn, map_act, map_lm_in;
   SkWorkspace sk;
   float *attn_ws_o = nullptr, *attn_ws_ml = nullptr;
+  int* attn_cnt = nullptr;
   size_t attn_ws_floats = 0;
   float2* rope = nullptr;
   // per-step metadata
@@ -467,6 +468,8 @@ void alloc_buffers(tc_instance* I) {
   I->attn_ws_floats = (size_t)kMaxDecodeItems * G * m.head_dim;
   TC_CUDA(cudaMalloc(&I->attn_ws_o, I->attn_ws_floats * 4));
   TC_CUDA(cudaMalloc(&I->attn_ws_ml, (size_t)kMaxDecodeItems * G * 2 * 4));
+  TC_CUDA(cudaMalloc(&I->attn_cnt, (size_t)S * m.n_kv_heads * 4));
+  TC_CUDA(cudaMemset(I->attn_cnt, 0, (size_t)S * m.n_kv_heads * 4));
   // RoPE table in fp64 -> fp32
   const int half = m.head_dim / 2;
   std::vector<float2> cs((size_t)I->desc.max_context * half);
@@ -543,10 +546,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
   if (n_dec > 0) {
     tc::attn_decode<DH, G><<<dec_grid, tc::kDecodeWarps * 32, tc::DecodeSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
     ++I->launches;
-    if (combine) {
-      tc::attn_decode_combine<DH, G><<<dim3(n_dec, I->d.n_heads), DH, 0, I->stream>>>(p);
-      ++I->launches;
-    }
+    (void)combine;  // split requests are merged inside attn_decode (last arriver)
   }
   TC_CUDA(cudaGetLastError());
 }
@@ -673,7 +673,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
         for (int c = 0; c < chunks; ++c) {
           int32_t* e = h + o_items + 4 * (size_t)it++;
           e[0] = n_pf + j;
-          e[1] = kh | (chunks == 1 ? (1 << 16) : 0);
+          e[1] = kh | (j << 8);
           e[2] = c * ppi;
           e[3] = std::min(pages, (c + 1) * ppi);
         }
@@ -716,6 +716,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   ap.dec_item_base = dm + o_ibase;
   ap.dec_chunks = dm + o_ichunks;
   ap.ws_o = I->attn_ws_o;
+  ap.dec_cnt = I->attn_cnt;
   ap.ws_ml = I->attn_ws_ml;
   tc::QkvRopeArgs rp{};
   rp.kv = I->kv;
@@ -729,7 +730,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   rp.n_kv_heads = m.n_kv_heads;
   rp.head_dim = m.head_dim;
   rp.page_size = ps;
-  const int rms_threads = 256;
+  constexpr int rms_threads = 256;
   for (int l = 0; l < m.n_layers; ++l) {
     const LayerW& L = I->layers[l];
     {
@@ -807,7 +808,7 @@ void destroy(tc_instance* I) {
     if (p) cudaFree(p);
   };
   f(I->weight_block); f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
-  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->rope); f(I->meta_dev);
+  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
   f(I->mig_dev);
   if (I->ids_host) cudaFreeHost(I->ids_host);
   if (I->meta_host) cudaFreeHost(I->meta_host);
