@@ -118,6 +118,44 @@ def cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=1):
             "seconds_per_step": sec, **det}
 
 
+def reduce_max(vals, device=None):
+    """Max over ranks of a list of floats (timing rule: multi-GPU numbers are the max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(vals)
+    t = torch.tensor(list(vals), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def simulated(args, rank, world, metric, config, P, D):
+    """CPU stand-in for the multi-rank path (gloo): same barrier / max-over-ranks / whole-job
+    aggregation as the GPU path, with a sleep in place of the step."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    for _ in range(args.warmup):
+        time.sleep(args.simulate_step_ms / 1e3)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(args.simulate_step_ms / 1e3 * (1 + 0.5 * rank))  # ranks deliberately unequal
+    local = time.perf_counter() - t0
+    (slowest,) = reduce_max([local])
+    if world > 1:
+        dist.barrier()
+    tokens = (P + D) * args.steps * world
+    if rank == 0:
+        print(json.dumps({"metric": metric, "value": tokens / slowest, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": slowest / args.steps * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "simulated": True,
+                          "data": "SIMULATED (test hook, no GPU)", "config": config, "rank_seconds_max": slowest}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -130,6 +168,9 @@ def main():
     ap.add_argument("--decode", type=int, default=64)
     ap.add_argument("--ctx", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--simulate-step-ms", type=float, default=0.0,
+                    help="TEST HOOK (CPU, gloo): replace the GPU step by a sleep to exercise the multi-rank "
+                         "timing / aggregation path; the output is marked simulated and is not a measurement")
     ap.add_argument("--profile-window", action="store_true",
                     help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off)")
     args = ap.parse_args()
@@ -174,6 +215,9 @@ def main():
 
     import torch
     import torch.distributed as dist
+
+    if args.simulate_step_ms > 0:
+        return simulated(args, rank, world, metric, config, P, D)
     from paper_2508_01989_b200 import Instance
 
     if world > 1:
@@ -223,10 +267,8 @@ def main():
     if args.profile_window:
         torch.cuda.profiler.stop()
     dev_s, wall_s = sum(gpu_ms) / 1e3, t1 - t0
+    dev_s, wall_s = reduce_max([dev_s, wall_s], device=f"cuda:{dev}")
     if world > 1:
-        t = torch.tensor([dev_s, wall_s], device=f"cuda:{dev}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s, wall_s = t.tolist()
         dist.barrier()
     tokens = (P + D) * args.steps * world
     value = tokens / dev_s

@@ -59,6 +59,14 @@ class GpuExecutor final : public pdsim::StepExecutor {
   }
 
   const std::vector<int32_t>& tokens(pdsim::RequestId rid) const { return reqs_[static_cast<size_t>(rid)].out; }
+
+  /// Wall-clock mode with several instances emulated on one GPU: a KV copy between two
+  /// instances on the same device runs HBM-to-HBM, faster than the NVLink it stands for, so
+  /// it is priced as bytes / link_gbps instead (0 = use the measured copy time).
+  void emulate_link(std::vector<int> devices, double link_gbps) {
+    devices_ = std::move(devices);
+    link_gbps_ = link_gbps;
+  }
   const ExecStats& stats() const { return stats_; }
 
   double launch_step(pdsim::InstanceId i, const pdsim::BatchPlan& plan, double, double model_ms) override {
@@ -127,7 +135,10 @@ class GpuExecutor final : public pdsim::StepExecutor {
     stats_.copy_ms += ms;
     stats_.copy_bytes += bytes;
     held_[static_cast<size_t>(from)].erase(rid);  // a token sampled mid-flight is discarded
-    return mode_ == ClockMode::Logical ? model_ms : static_cast<double>(ms);
+    if (mode_ == ClockMode::Logical) return model_ms;
+    const bool same_dev = !devices_.empty() && devices_[static_cast<size_t>(from)] == devices_[static_cast<size_t>(to)];
+    if (same_dev && link_gbps_ > 0.0) return static_cast<double>(bytes) / (link_gbps_ * 1e6);
+    return static_cast<double>(ms);
   }
 
   void request_done(pdsim::RequestId rid, pdsim::InstanceId i) override {
@@ -168,6 +179,8 @@ class GpuExecutor final : public pdsim::StepExecutor {
   std::vector<tc_decode_item> decodes_;
   std::vector<int32_t> ids_;
   ExecStats stats_;
+  std::vector<int> devices_;
+  double link_gbps_ = 0.0;
 };
 
 }  // namespace taichi

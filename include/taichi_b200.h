@@ -55,6 +55,8 @@ typedef struct {
   float rms_eps;
 } tc_model_dims;
 
+typedef struct tc_instance tc_instance;
+
 /* Presets: "tiny", "llama3_8b", "qwen2_5_14b".
  * Optional suffix ":L<n>" overrides the layer count (layer-reduced oracle runs). */
 tc_status tc_model_preset(const char* name, tc_model_dims* out);
@@ -68,9 +70,9 @@ typedef struct {
   int32_t max_step_tokens;   /* max packed rows per step (prefill + decode) */
   int32_t max_seqs;          /* max sequences (slices + decodes) per step */
   int32_t max_context;       /* max position + 1 (RoPE table size) */
+  const struct tc_instance* share_weights; /* optional: reuse this instance's weights (same device,
+                                              dims and seed) -- several instances on one GPU */
 } tc_instance_desc;
-
-typedef struct tc_instance tc_instance;
 
 tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out);
 tc_status tc_instance_destroy(tc_instance* inst);

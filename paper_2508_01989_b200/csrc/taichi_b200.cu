@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <string>
@@ -299,8 +300,8 @@ struct tc_instance {
   tc_model_dims d{};
   int sms = 0;
   cudaStream_t stream = nullptr;
-  // weights
-  void* weight_block = nullptr;
+  // weights (shared_ptr: instances on one GPU may share one replica)
+  std::shared_ptr<void> weight_owner;
   __nv_bfloat16 *embed = nullptr, *final_norm = nullptr;
   WMat lm_head;
   std::vector<LayerW> layers;
@@ -399,8 +400,14 @@ void alloc_weights(tc_instance* I) {
   size_t per_layer = al(I->qkv_n * dm * 2) + al(dm * H * dh * 2) + al(2 * F * dm * 2) + al(dm * F * 2) +
                      al(I->qkv_n * 2) + 2 * al(dm * 2);
   size_t total = 2 * al(V * dm * 2) + al(dm * 2) + per_layer * m.n_layers;
-  TC_CUDA(cudaMalloc(&I->weight_block, total));
-  uint8_t* cur = static_cast<uint8_t*>(I->weight_block);
+  void* block = nullptr;
+  TC_CUDA(cudaMalloc(&block, total));
+  const int dev = I->desc.device;
+  I->weight_owner = std::shared_ptr<void>(block, [dev](void* p) {
+    DeviceGuard g(dev);
+    cudaFree(p);
+  });
+  uint8_t* cur = static_cast<uint8_t*>(block);
   cudaStream_t s = I->stream;
   const uint64_t seed = I->desc.weight_seed;
   I->embed = (__nv_bfloat16*)carve(cur, V * dm * 2);
@@ -807,7 +814,8 @@ void destroy(tc_instance* I) {
   auto f = [](void* p) {
     if (p) cudaFree(p);
   };
-  f(I->weight_block); f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
+  I->weight_owner.reset();
+  f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
   f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
   f(I->mig_dev);
   if (I->ids_host) cudaFreeHost(I->ids_host);
@@ -925,7 +933,20 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     I->sms = device_sms(desc->device);
     init_kernel_attrs(desc->device);
     TC_CUDA(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
-    alloc_weights(I);
+    if (desc->share_weights) {
+      const tc_instance* o = desc->share_weights;
+      TC_REQUIRE(o->desc.device == desc->device, "create: share_weights needs the same device");
+      TC_REQUIRE(std::memcmp(&o->d, &desc->dims, sizeof(tc_model_dims)) == 0 && o->desc.weight_seed == desc->weight_seed,
+                 "create: share_weights needs identical dims and seed");
+      I->weight_owner = o->weight_owner;
+      I->embed = o->embed;
+      I->final_norm = o->final_norm;
+      I->lm_head = o->lm_head;
+      I->layers = o->layers;
+      I->qkv_n = o->qkv_n;
+    } else {
+      alloc_weights(I);
+    }
     alloc_buffers(I);
     const tc_model_dims& m = I->d;
     I->page_elems = (int64_t)m.n_layers * 2 * m.n_kv_heads * desc->page_size * m.head_dim;

@@ -2,14 +2,17 @@
 //
 //   taichi_serve --config F [--seed S] [--model tiny|llama3_8b|qwen2_5_14b[:Ln]]
 //                [--devices 0,1,..] [--clock logical|wall] [--pool-tokens N]
-//                [--log OUT] [--tokens OUT.jsonl]
+//                [--log OUT] [--tokens OUT.jsonl] [--share-weights 0|1] [--link-gbps G]
 //
 // --clock logical: the cost model prices every step/transfer (schedule byte-identical to the
 //   reference's, checked against the oracle log) while every step really runs on the GPU and
 //   every migration really copies KV pages; tokens are written per request for the oracle.
 // --clock wall: measured device step / copy times drive the clock (real SLO goodput).
-// Instances are placed round-robin on --devices (one per GPU in production; several may
-// share a GPU in tests).
+// Instances are placed round-robin on --devices (one per GPU in production). Several
+// instances may share a GPU (tests, or emulating an 8-GPU box on one B200): they then share
+// one weight replica, each step is still executed and timed alone (steps run synchronously in
+// event order), and in wall mode a same-device KV copy is priced at --link-gbps (default 770,
+// the measured B200 NVLink peer-copy bandwidth) instead of its HBM-local copy time.
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -36,6 +39,8 @@ int main(int argc, char** argv) {
   using namespace pdsim;
   std::string config, model = "tiny", devices = "0", clock = "logical", log, tokens_out;
   long long seed = -1, pool_tokens = 0;
+  int share_weights = 1;
+  double link_gbps = 770.0;
   unsigned long long weight_seed = 1;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
@@ -48,6 +53,8 @@ int main(int argc, char** argv) {
     else if (k == "--log") log = v;
     else if (k == "--tokens") tokens_out = v;
     else if (k == "--weight-seed") weight_seed = std::stoull(v);
+    else if (k == "--share-weights") share_weights = std::stoi(v);
+    else if (k == "--link-gbps") link_gbps = std::stod(v);
     else {
       std::fprintf(stderr, "unknown flag %s\n", k.c_str());
       return 2;
@@ -71,6 +78,7 @@ int main(int argc, char** argv) {
     }
     const std::vector<int> devs = parse_ints(devices);
     if (devs.empty()) throw ConfigError("--devices: empty");
+    std::vector<int> inst_dev;
     for (std::size_t i = 0; i < in.instances.size(); ++i) {
       const InstanceSpec& sp = in.instances[i];
       tc_instance_desc d{};
@@ -86,11 +94,20 @@ int main(int argc, char** argv) {
       d.max_step_tokens = static_cast<int32_t>(std::max<Tokens>(sp.chunk_size, 1) + 1024);
       d.max_seqs = 1024;
       d.max_context = static_cast<int32_t>(max_ctx + 16);
+      d.share_weights = nullptr;
+      if (share_weights)
+        for (std::size_t j = 0; j < insts.size(); ++j)
+          if (inst_dev[j] == d.device) {
+            d.share_weights = insts[j];
+            break;
+          }
+      inst_dev.push_back(d.device);
       tc_instance* h = nullptr;
       taichi::tc_check(tc_instance_create(&d, &h), "tc_instance_create");
       insts.push_back(h);
     }
     taichi::GpuExecutor exec(insts, recs, dims.vocab, s, clock == "wall" ? taichi::ClockMode::Wall : taichi::ClockMode::Logical);
+    exec.emulate_link(inst_dev, link_gbps);
     in.executor = &exec;
     FILE* f = log.empty() ? nullptr : std::fopen(log.c_str(), "w");
     long long plans = 0;
@@ -119,10 +136,12 @@ int main(int argc, char** argv) {
         "{\"iterations\": %lld, \"requests\": %zu, \"attainment\": %.17g, \"p90_ttft_ms\": %.17g, "
         "\"p90_tpot_ms\": %.17g, \"migrations_init\": %lld, \"migrations_degrade\": %lld, "
         "\"migrations_backflow\": %lld, \"sim_end_ms\": %.17g, \"gpu_steps\": %lld, \"gpu_step_ms\": %.6f, "
-        "\"gpu_launches\": %lld, \"kv_copies\": %lld, \"kv_copy_ms\": %.6f, \"kv_copy_bytes\": %lld, \"clock\": \"%s\"}\n",
+        "\"gpu_launches\": %lld, \"kv_copies\": %lld, \"kv_copy_ms\": %.6f, \"kv_copy_bytes\": %lld, \"clock\": \"%s\", "
+        "\"link_gbps_same_device\": %.1f, \"p50_ttft_ms\": %.17g, \"p50_tpot_ms\": %.17g}\n",
         plans, sim.lifecycles.size(), rep.agg.attainment, rep.agg.p90_ttft_ms, rep.agg.p90_tpot_ms,
         sim.migrations_init, sim.migrations_degrade, sim.migrations_backflow, sim.sim_end_ms, st.steps,
-        st.step_gpu_ms, st.launches, st.migrations, st.copy_ms, st.copy_bytes, clock.c_str());
+        st.step_gpu_ms, st.launches, st.migrations, st.copy_ms, st.copy_bytes, clock.c_str(), link_gbps,
+        rep.agg.p50_ttft_ms, rep.agg.p50_tpot_ms);
   } catch (const ConfigError& e) {
     std::fprintf(stderr, "config error: %s\n", e.what());
     rc = 1;

@@ -44,7 +44,7 @@ class ModelDims(C.Structure):
 class _InstanceDesc(C.Structure):
     _fields_ = [("device", C.c_int32), ("dims", ModelDims), ("weight_seed", C.c_uint64),
                 ("page_size", C.c_int32), ("kv_pool_tokens", C.c_int64), ("max_step_tokens", C.c_int32),
-                ("max_seqs", C.c_int32), ("max_context", C.c_int32)]
+                ("max_seqs", C.c_int32), ("max_context", C.c_int32), ("share_weights", C.c_void_p)]
 
 
 class _PrefillSlice(C.Structure):
@@ -137,11 +137,12 @@ class Instance:
 
     def __init__(self, model: str | ModelDims = "tiny", device: int = 0, weight_seed: int = 0,
                  kv_pool_tokens: int = 1 << 16, max_step_tokens: int = 2048, max_seqs: int = 256,
-                 max_context: int = 4096, page_size: int = 16):
+                 max_context: int = 4096, page_size: int = 16, share_weights: "Instance | None" = None):
         lib = load_library()
         self.dims = model_preset(model) if isinstance(model, str) else model
         desc = _InstanceDesc(device, self.dims, weight_seed, page_size, kv_pool_tokens, max_step_tokens,
-                             max_seqs, max_context)
+                             max_seqs, max_context, share_weights._h.value if share_weights is not None else None)
+        self._shared_from = share_weights  # keep the owner alive
         h = C.c_void_p()
         _check(lib.tc_instance_create(C.byref(desc), C.byref(h)))
         self._h = h

@@ -91,3 +91,20 @@ def test_migration_heavy_serving(built, cuda_ok, oracle_model, tmp_path):
     assert len(migrated) > 100
     picked = [r for r in rec if r["id"] in migrated][:40]
     check_tokens(oracle_model, 0, picked)
+
+
+def test_wall_clock_mode_runs_on_measured_times(built, cuda_ok, tmp_path):
+    """Wall-clock mode: measured device times drive the clock (decisions may legitimately differ
+    from the cost-model schedule); every request completes and the clock advanced by the
+    measured step times."""
+    log, toks = tmp_path / "w.log", tmp_path / "w.jsonl"
+    p = subprocess.run([str(built / "taichi_serve"), "--config", str(REPO / "configs" / "c1_tiny_hybrid.json"),
+                        "--model", "tiny", "--devices", "0", "--clock", "wall", "--pool-tokens", "200000",
+                        "--log", str(log), "--tokens", str(toks)], capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr
+    s = json.loads(p.stdout)
+    assert s["clock"] == "wall" and s["requests"] == 64
+    busy = sum(float.fromhex(l.split()[4]) for l in log.read_text().splitlines() if l.startswith("I "))
+    assert abs(busy - s["gpu_step_ms"]) < 1e-3 * max(1.0, busy)  # busy time == measured device time
+    for r in (json.loads(l) for l in toks.read_text().splitlines()):
+        assert len(r["tokens"]) >= 1

@@ -235,3 +235,28 @@ def test_llama_shape_mixed_step(llama_l2):
         follow[rid].check(int(out.sampled[1 + k]), out.logits[1 + k])
     for rid in list(prompts) + [500, 501]:
         inst.kv_release(rid)
+
+
+def test_qwen_shape_bias_and_group5():
+    """Qwen2.5-14B layer shapes (2 layers, vocab 152064): QKV bias, GQA group 5 (40 q / 8 kv heads)."""
+    from paper_2508_01989_b200 import Instance
+    with Instance("qwen2_5_14b:L2", weight_seed=5, kv_pool_tokens=1 << 14, max_step_tokens=1024, max_seqs=32,
+                  max_context=4096) as inst:
+        d = mr.preset("qwen2_5_14b:L2")
+        model = mr.RefModel(d, mr.weights_from_device(inst, d), max_pos=4096)
+        prompts = {rid: mr.prompt_tokens(5, rid, 300 + 97 * rid, d.vocab) for rid in range(3)}
+        out = inst.step(prefill=[(rid, 0, p, True) for rid, p in prompts.items()], keep_logits=True)
+        follow = {}
+        for k, (rid, p) in enumerate(prompts.items()):
+            follow[rid] = Follower(model, p)
+            follow[rid].check(int(out.sampled[k]), out.logits[k])
+        toks = {rid: int(out.sampled[k]) for k, rid in enumerate(prompts)}
+        pos = {rid: len(p) for rid, p in prompts.items()}
+        for _ in range(3):
+            dec = [(rid, pos[rid], toks[rid]) for rid in prompts]
+            o = inst.step(decode=dec, keep_logits=True)
+            for k, (rid, _, tok) in enumerate(dec):
+                follow[rid].feed([tok])
+                follow[rid].check(int(o.sampled[k]), o.logits[k])
+                toks[rid] = int(o.sampled[k])
+                pos[rid] += 1
