@@ -67,6 +67,15 @@ def build_host(force: bool = False) -> pathlib.Path:
     return out
 
 
+def build_cuda_variant(name: str, defines: list[str]) -> pathlib.Path:
+    """Extra library builds for A/B microbenchmarks (e.g. TC_GEMM_BK=64); not used by the product."""
+    out = LIB / f"libtaichi_b200_{name}.so"
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [INCLUDE / "taichi_b200.h"]
+    if _stale(out, deps):
+        _run([NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{INCLUDE}", CSRC / "taichi_b200.cu", "-o", out])
+    return out
+
+
 def build_serve(force: bool = False) -> pathlib.Path:
     """Host engine + GPU executor, linked against lib/libtaichi_b200.so (rpath $ORIGIN)."""
     out = LIB / "taichi_serve"

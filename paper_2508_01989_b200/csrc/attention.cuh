@@ -4,9 +4,10 @@
 //   pool[page][layer][k|v][kv_head][slot 0..PS-1][head_dim]   (bf16, PS = 16)
 // One (page, layer, k|v, kv_head) block is 16 rows x head_dim, 4 KiB contiguous for
 // head_dim 128. It is fetched by ONE TMA instruction through a 3-D tensor map
-// {64 dims, head_dim/64 halves, pool rows} with 128 B swizzle, which lands it in
-// shared memory bank-conflict free for ldmatrix (address = line*128 +
-// ((chunk ^ line) & 7) * 16). Completion is tracked with mbarrier transaction
+// {64 dims, pool rows, head_dim/64 halves} (strides 256 B, 128 B) with 128 B swizzle:
+// each 64-dim half lands as its own 16-line slab (the K-major SW128 layout), so the
+// 8 keys of an ldmatrix phase hit 8 distinct bank groups
+// (address = half*2048 + key*128 + ((chunk ^ key) & 7) * 16). Completion is tracked with mbarrier transaction
 // counts, so no thread computes per-chunk gather addresses.
 //
 //  * attn_prefill  -- chunked-prefill queries (a chunk may span prompts; each slice
@@ -84,8 +85,9 @@ struct KvBlock {
 // Swizzled smem address of (key, col) inside consecutive page blocks starting at base.
 template <int DH>
 TC_DEVICE uint32_t kv_addr(uint32_t base, int key, int col) {
-  const int line = (key & (kPage - 1)) * KvBlock<DH>::kHalves + (col >> 6);
-  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + line * 128 + ((((col & 63) >> 3) ^ (line & 7)) << 4));
+  const int row = key & (kPage - 1);
+  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + (col >> 6) * (kPage * 128) + row * 128 +
+                           ((((col & 63) >> 3) ^ (row & 7)) << 4));
 }
 
 // Pool row of (page, layer, k|v, head, slot 0) for the 3-D tensor map.
@@ -254,9 +256,9 @@ __global__ void __launch_bounds__(kPrefillThreads) attn_prefill(const __grid_con
         for (int pg = 0; pg < kTilePages; ++pg) {
           const int gp = t * kTilePages + pg;
           const int page = bt[gp < n_pages ? gp : 0];  // beyond the sequence: any valid page, masked
-          tma_load_3d(dst + pg * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, 0, kv_row(p, page, 0, kvh));
-          tma_load_3d(dst + (kTilePages + pg) * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, 0,
-                      kv_row(p, page, 1, kvh));
+          tma_load_3d(dst + pg * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, kv_row(p, page, 0, kvh), 0);
+          tma_load_3d(dst + (kTilePages + pg) * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, kv_row(p, page, 1, kvh),
+                      0);
         }
       }
     }
@@ -351,8 +353,8 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_co
         const uint32_t dst = wbase + st * DecodeSmem<DH>::kStageBytes;
         fence_proxy_async();
         mbar_arrive_expect_tx(&full[st], DecodeSmem<DH>::kStageBytes);
-        tma_load_3d(dst, &kv_map, &full[st], 0, 0, kv_row(p, page, 0, kvh));
-        tma_load_3d(dst + KvBlock<DH>::kBytes, &kv_map, &full[st], 0, 0, kv_row(p, page, 1, kvh));
+        tma_load_3d(dst, &kv_map, &full[st], 0, kv_row(p, page, 0, kvh), 0);
+        tma_load_3d(dst + KvBlock<DH>::kBytes, &kv_map, &full[st], 0, kv_row(p, page, 1, kvh), 0);
         ++issued;
         ++l_page;
         return;

@@ -118,15 +118,18 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);          // M / 16
 }
 
-// Shared-memory matrix descriptor: K-major tile whose rows are 128 B (64 bf16),
-// SWIZZLE_128B as written by TMA; 8-row core-matrix groups are 1024 B apart.
-TC_DEVICE uint64_t umma_smem_desc_sw128(uint32_t smem_addr) {
+// Shared-memory matrix descriptor of a K-major tile as written by TMA with a
+// ROW_BYTES-wide swizzle (128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B): rows of
+// ROW_BYTES, 8-row core-matrix groups 8 * ROW_BYTES apart.
+template <int ROW_BYTES>
+TC_DEVICE uint64_t umma_smem_desc(uint32_t smem_addr) {
+  static_assert(ROW_BYTES == 128 || ROW_BYTES == 64, "supported swizzles: 128B, 64B");
   uint64_t d = 0;
-  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);  // start address
-  d |= (uint64_t)1 << 16;                       // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;             // SBO = 1024 B
-  d |= (uint64_t)1 << 46;                       // descriptor version (sm100)
-  d |= (uint64_t)2 << 61;                       // layout: SWIZZLE_128B
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);          // start address
+  d |= (uint64_t)1 << 16;                               // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)((8 * ROW_BYTES) >> 4) << 32;          // SBO
+  d |= (uint64_t)1 << 46;                               // descriptor version (sm100)
+  d |= (uint64_t)(ROW_BYTES == 128 ? 2 : 4) << 61;      // layout: SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
 

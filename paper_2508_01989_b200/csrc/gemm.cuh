@@ -21,8 +21,10 @@
 // No CTA ever waits for another, so concurrent streams on one GPU cannot deadlock.
 //
 // Warp roles (256 threads, 1 CTA/SM):
-//   warp 0      TMA producer: A/B K-slabs (BK = 64 -> 128 B rows, SWIZZLE_128B)
-//               into a kStages-deep smem ring guarded by full/empty mbarriers.
+//   warp 0      TMA producer: A/B K-slabs (BK = 32 -> 64 B rows, SWIZZLE_64B) into a
+//               deep smem ring (8 stages at BN = 256: 7 x 24 KB in flight covers the
+//               ~1 us TMA latency at the MMA consumption rate) guarded by full/empty
+//               mbarriers.
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128, N=BN,
 //               K=16) into a double-buffered TMEM accumulator; tcgen05.commit
 //               releases smem slots and signals the epilogue.
@@ -59,7 +61,10 @@ struct QkvRopeArgs {
 };
 
 constexpr int kGemmBM = 128;
-constexpr int kGemmBK = 64;
+#ifndef TC_GEMM_BK
+#define TC_GEMM_BK 32
+#endif
+constexpr int kGemmBK = TC_GEMM_BK;  // K per pipeline stage (32 or 64 bf16 = 64 / 128 B rows)
 constexpr int kGemmThreads = 256;
 
 struct GemmArgs {
@@ -73,17 +78,19 @@ struct GemmArgs {
   float* ws;                 // partial slots [units][BN/32][128][32] (splits > 1)
   int* tile_cnt;             // per-tile arrival counters (zero; last arriver resets)
   QkvRopeArgs rope;          // EPI_QKV_ROPE only
+  float* red_out;            // small-M streaming mode: every unit red.adds its partial into this
+                             // zeroed fp32 [M, N] scratch; a finish kernel applies the epilogue
 };
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static constexpr int kStages = (BN >= 256 ? 4 : 6) * (64 / kGemmBK);
   static constexpr int kABytes = kGemmBM * kGemmBK * 2;
   static constexpr int kBBytes = BN * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kSlotFloats = kGemmBM * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -328,8 +335,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
-            const uint64_t ad = umma_smem_desc_sw128(a_addr + k * 32);
-            const uint64_t bd = umma_smem_desc_sw128(b_addr + k * 32);
+            const uint64_t ad = umma_smem_desc<kGemmBK * 2>(a_addr + k * 32);
+            const uint64_t bd = umma_smem_desc<kGemmBK * 2>(b_addr + k * 32);
             umma_bf16(d_tmem, ad, bd, idesc, (kb > k0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);
@@ -359,6 +366,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m = mt * kGemmBM + row;
       const bool row_ok = m < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (args.red_out != nullptr) {  // streaming mode (decode-only steps): accumulate and move on
+#pragma unroll 1
+        for (int chunk = 0; chunk < BN / 32; ++chunk) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + chunk * 32, r);
+          tmem_ld_wait();
+          if (row_ok) {
+            float* dst = args.red_out + (size_t)m * args.N + nt * BN + chunk * 32;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + q * 4),
+                           "f"(__uint_as_float(r[q * 4])), "f"(__uint_as_float(r[q * 4 + 1])),
+                           "f"(__uint_as_float(r[q * 4 + 2])), "f"(__uint_as_float(r[q * 4 + 3]))
+                           : "memory");
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty_bar[acc]);
+        continue;
+      }
       // residual-add GEMMs reduce split-K partials with red.global.add (no workspace)
       const bool whole = args.splits == 1 || EPI == EPI_RESID_F32;
 
@@ -480,6 +507,65 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------- streaming-mode finishers
+// SwiGLU over the fp32 scratch of a 64-interleaved gate|up GEMM: act[m, j] = silu(g) * u.
+__global__ void finish_swiglu(const float* __restrict__ scr, int M, int F, __nv_bfloat16* __restrict__ act) {
+  const long long n4 = (long long)M * F / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 4;
+    const int m = (int)(e / F), j = (int)(e % F);
+    const float* row = scr + (size_t)m * 2 * F;
+    const int gc = (j / 64) * 128 + (j % 64);
+    const float4 g = *reinterpret_cast<const float4*>(row + gc);
+    const float4 u = *reinterpret_cast<const float4*>(row + gc + 64);
+    uint2 w;
+    w.x = pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y);
+    w.y = pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w);
+    *reinterpret_cast<uint2*>(act + (size_t)m * F + j) = w;
+  }
+}
+
+// (+bias) -> RoPE(q, k) -> q into q_out, k / v into the paged pool; one thread per
+// (row, head, rotation pair j < head_dim / 2).
+__global__ void finish_qkv_rope(const float* __restrict__ scr, int M, QkvRopeArgs r, const __nv_bfloat16* bias,
+                                __nv_bfloat16* __restrict__ q_out, int q_ld) {
+  const int half = r.head_dim / 2;
+  const int heads = r.n_heads + 2 * r.n_kv_heads;
+  const int N = heads * r.head_dim;
+  const long long total = (long long)M * heads * half;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % half);
+    const int head = (int)((i / half) % heads);
+    const int m = (int)(i / ((long long)half * heads));
+    const int c = head * r.head_dim + j;
+    float lo = scr[(size_t)m * N + c], hi = scr[(size_t)m * N + c + half];
+    if (bias) {
+      lo += __bfloat162float(bias[c]);
+      hi += __bfloat162float(bias[c + half]);
+    }
+    const int pos = r.positions[m];
+    const bool is_q = head < r.n_heads, is_k = !is_q && head < r.n_heads + r.n_kv_heads;
+    if (is_q || is_k) {
+      const float2 cs = r.rope_cs[(size_t)pos * half + j];
+      const float a = lo, b = hi;
+      lo = a * cs.x - b * cs.y;
+      hi = b * cs.x + a * cs.y;
+    }
+    __nv_bfloat16* dst;
+    if (is_q) {
+      dst = q_out + (size_t)m * q_ld + head * r.head_dim;
+    } else {
+      const int seq = r.row_seq[m];
+      const int page = r.block_tables[r.seq_bt_off[seq] + pos / r.page_size];
+      const int kvh = head - r.n_heads - (is_k ? 0 : r.n_kv_heads);
+      dst = r.kv + (size_t)page * r.page_stride +
+            ((((size_t)r.layer * 2 + (is_k ? 0 : 1)) * r.n_kv_heads + kvh) * r.page_size + pos % r.page_size) * r.head_dim;
+    }
+    dst[j] = __float2bfloat16(lo);
+    dst[j + half] = __float2bfloat16(hi);
   }
 }
 

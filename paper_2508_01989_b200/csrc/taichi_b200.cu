@@ -87,17 +87,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// Row-major bf16 [rows, cols] matrix, box = 64 (K) x box_rows, 128 B swizzle.
+// Row-major bf16 [rows, cols] GEMM operand, box = kGemmBK (K) x box_rows, swizzle = row bytes.
 CUtensorMap make_kmajor_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {cols * 2};
-  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)tc::kGemmBK, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                          tc::kGemmBK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw TcFail{TC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
   return m;
 }
@@ -156,10 +156,30 @@ struct GemmChoice {
 //    last-arriver reduction land in the tail of the wave.
 //  * M <= 128 (decode-only steps, weight streaming): 128-wide tiles split 3 ways when fewer
 //    than half the SMs would get a tile (qkv 23 -> 21 us, down 66 -> 41 us at M = 64).
-GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits) {
+GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits, bool streaming = false) {
   GemmChoice c{};
   c.m_tiles = (M + tc::kGemmBM - 1) / tc::kGemmBM;
   c.kb = K / tc::kGemmBK;
+  if (streaming && !force_bn && !force_splits) {
+    // decode-only steps (M <= 128): the GEMM is a weight stream. Pick splits so every SM streams
+    // (~40 GB/s per SM) with few waves: t = weight bytes / (active SMs * 40 GB/s) + 2 us per wave.
+    c.bn = (N % 256 == 0) ? 256 : 128;
+    c.n_tiles = N / c.bn;
+    const long long tiles = (long long)c.m_tiles * c.n_tiles;
+    double best = 1e30;
+    for (int sp = 1; sp <= std::min(16, std::max(1, c.kb / 4)); ++sp) {
+      const long long units = tiles * sp, active = std::min<long long>(units, sms);
+      const long long waves = (units + sms - 1) / sms;
+      const double t = (double)N * K * 2 / (active * 40.0e3) + 2.0 * waves;
+      if (t < best - 1e-9) {
+        best = t;
+        c.splits = sp;
+      }
+    }
+    c.grid = (int)std::min<long long>(sms, tiles * c.splits);
+    c.est_us = best;
+    return c;
+  }
   if (force_bn) c.bn = force_bn;
   else if (epi != tc::EPI_RESID_F32 && M <= tc::kGemmBM && (long long)c.m_tiles * (N / 128) < sms / 2) c.bn = 128;
   else c.bn = (N % 256 == 0) ? 256 : 128;
@@ -228,12 +248,12 @@ struct SkWorkspace {
 // out = epi(A[M,K] * W[N,K]^T). a_map: box 128 rows over the activation buffer.
 int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
              int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
-             const tc::QkvRopeArgs* rope = nullptr) {
+             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr) {
   const int N = (int)w.rows, K = (int)w.cols;
-  TC_REQUIRE(K % tc::kGemmBK == 0, "gemm: K must be a multiple of 64");
+  TC_REQUIRE(K % 64 == 0, "gemm: K must be a multiple of 64");
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
   TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256, "gemm: tile width must be 128 or 256");
-  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits);
+  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits, red_out != nullptr);
   TC_REQUIRE((long long)c.m_tiles * c.n_tiles <= kSkMaxTiles, "gemm: too many tiles");
   tc::GemmArgs args{};
   args.M = M;
@@ -249,7 +269,8 @@ int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo,
   args.bias = bias;
   args.ws = sk.ws;
   args.tile_cnt = sk.cnt;
-  if (epi == tc::EPI_QKV_ROPE) {
+  args.red_out = red_out;
+  if (epi == tc::EPI_QKV_ROPE && red_out == nullptr) {
     TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
     TC_REQUIRE(c.bn % rope->head_dim == 0, "gemm: tile width must cover whole heads");
     args.rope = *rope;
@@ -267,6 +288,7 @@ struct LayerW {
 };
 
 constexpr int kMaxDecodeItems = 16384;
+constexpr int kStreamRows = 128;  // steps with <= this many rows run their QKV / gate_up GEMMs in streaming mode
 
 constexpr uint64_t kTidEmbed = 1, kTidLmHead = 2, kTidFinalNorm = 3;
 inline uint64_t tid_layer(int l, int j) { return 16 + 16ull * l + j; }
@@ -320,6 +342,7 @@ struct tc_instance {
   int* ids_host = nullptr;
   CUtensorMap map_xnorm, map_attn, map_act, map_lm_in;
   SkWorkspace sk;
+  float* stream_scr = nullptr;  // fp32 [<=128, max(qkv_n, 2F)] accumulation scratch (decode-only steps)
   float *attn_ws_o = nullptr, *attn_ws_ml = nullptr;
   int* attn_cnt = nullptr;
   size_t attn_ws_floats = 0;
@@ -466,6 +489,7 @@ void alloc_buffers(tc_instance* I) {
   I->map_attn = make_kmajor_map(I->attn_out, Tp, (uint64_t)m.n_heads * m.head_dim, 128);
   I->map_act = make_kmajor_map(I->act, Tp, m.ffn_dim, 128);
   I->map_lm_in = make_kmajor_map(I->lm_in, Sp, dm, 128);
+  TC_CUDA(cudaMalloc(&I->stream_scr, (size_t)kStreamRows * std::max<int64_t>(I->qkv_n, 2 * (int64_t)m.ffn_dim) * 4));
   // stream-K partial slots + tile counters (counters must start at zero)
   TC_CUDA(cudaMalloc(&I->sk.ws, kSkWsBytes));
   TC_CUDA(cudaMalloc(&I->sk.cnt, (size_t)kSkMaxTiles * 4));
@@ -738,19 +762,32 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   rp.head_dim = m.head_dim;
   rp.page_size = ps;
   constexpr int rms_threads = 256;
+  // decode-heavy steps: QKV / gate_up stream their weights over every SM (split-K, red.add into a
+  // zeroed fp32 scratch) and a finish kernel applies RoPE + KV append / SwiGLU
+  const bool streaming = T <= kStreamRows;
+  const int fin_blocks = 2 * I->sms;
   for (int l = 0; l < m.n_layers; ++l) {
     const LayerW& L = I->layers[l];
     {
       ProfScope p_(I, "norm");
-      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps);
+      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps,
+                                                              streaming ? I->stream_scr : nullptr, I->qkv_n);
       ++I->launches;
     }
     {
       // QKV projection with fused bias, RoPE and paged KV append (q stays in I->qkv)
       ProfScope p_(I, "gemm_qkv");
       rp.layer = l;
-      I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
-                              tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp);
+      if (streaming) {
+        I->launches += run_gemm(I->map_xnorm, L.qkv, T, nullptr, I->qkv_n, nullptr, tc::EPI_BF16, I->sms, I->sk, s, 0, 0,
+                                nullptr, I->stream_scr);
+        tc::finish_qkv_rope<<<fin_blocks, 256, 0, s>>>(I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
+                                                      I->qkv_n);
+        ++I->launches;
+      } else {
+        I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
+                                tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp);
+      }
     }
     {
       ProfScope p_(I, "attn");
@@ -763,12 +800,20 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "norm");
-      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps);
+      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps,
+                                                              streaming ? I->stream_scr : nullptr, 2 * m.ffn_dim);
       ++I->launches;
     }
     {
       ProfScope p_(I, "gemm_gate_up");
-      I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
+      if (streaming) {
+        I->launches += run_gemm(I->map_xnorm, L.gate_up, T, nullptr, m.ffn_dim, nullptr, tc::EPI_BF16, I->sms, I->sk, s,
+                                0, 0, nullptr, I->stream_scr);
+        tc::finish_swiglu<<<fin_blocks, 256, 0, s>>>(I->stream_scr, T, m.ffn_dim, I->act);
+        ++I->launches;
+      } else {
+        I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
+      }
     }
     {
       ProfScope p_(I, "gemm_down");
@@ -816,7 +861,7 @@ void destroy(tc_instance* I) {
   };
   I->weight_owner.reset();
   f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
-  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
+  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->stream_scr); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
   f(I->mig_dev);
   if (I->ids_host) cudaFreeHost(I->ids_host);
   if (I->meta_host) cudaFreeHost(I->meta_host);
@@ -956,9 +1001,11 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     {
       const uint64_t rows = (uint64_t)I->n_pages * m.n_layers * 2 * m.n_kv_heads * desc->page_size;
       TC_REQUIRE(rows < (1ull << 31), "create: KV pool too large for 32-bit TMA row coordinates");
-      const cuuint64_t dims[3] = {64, (cuuint64_t)(m.head_dim / 64), rows};
-      const cuuint64_t strides[2] = {128, (cuuint64_t)m.head_dim * 2};
-      const cuuint32_t box[3] = {64, (cuuint32_t)(m.head_dim / 64), (cuuint32_t)desc->page_size};
+      // dims {64 dims, pool rows, head_dim/64 halves}: each half of a 16-row block lands as a
+      // separate 16-line 128 B-swizzled slab (bank-conflict-free ldmatrix, K-major SW128 layout)
+      const cuuint64_t dims[3] = {64, rows, (cuuint64_t)(m.head_dim / 64)};
+      const cuuint64_t strides[2] = {(cuuint64_t)m.head_dim * 2, 128};
+      const cuuint32_t box[3] = {64, (cuuint32_t)desc->page_size, (cuuint32_t)(m.head_dim / 64)};
       const cuuint32_t estr[3] = {1, 1, 1};
       const CUresult r = tensor_map_encoder()(&I->kv_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, I->kv, dims, strides, box,
                                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -75,7 +75,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = pathlib.Path(path) if path else LIB_PATH
+    p = pathlib.Path(path) if path else pathlib.Path(os.environ.get("TAICHI_B200_LIB", LIB_PATH))
     if not p.exists():
         raise FileNotFoundError(f"{p} missing: the CUDA library is not built (no CPU fallback exists)")
     lib = C.CDLL(str(p))
