@@ -39,7 +39,7 @@ struct AttnParams {
   const int* block_tables;   // flat page ids
   const int* qblk_seq;       // prefill work list
   const int* qblk_off;
-  const int4* dec_items;     // decode work: (seq, kvh | decode index << 8, page0, page1)
+  const int4* dec_items;     // decode work: (block-table offset, kvh | decode index << 8, page0, page1)
   int n_items;
   const int* dec_seq;        // decode index -> sequence
   const int* dec_item_base;  // decode index -> first item; items (d, kvh, j) at base + kvh * chunks + j
@@ -82,13 +82,27 @@ struct KvBlock {
   static constexpr int kHalves = DH / 64;
 };
 
+#ifndef TC_KV_SLAB
+#define TC_KV_SLAB 1  // 1: {64, rows, halves} box (one slab per half); 0: {64, halves, rows} (interleaved)
+#endif
 // Swizzled smem address of (key, col) inside consecutive page blocks starting at base.
 template <int DH>
 TC_DEVICE uint32_t kv_addr(uint32_t base, int key, int col) {
   const int row = key & (kPage - 1);
+#if TC_KV_SLAB
   return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + (col >> 6) * (kPage * 128) + row * 128 +
                            ((((col & 63) >> 3) ^ (row & 7)) << 4));
+#else
+  const int line = row * KvBlock<DH>::kHalves + (col >> 6);
+  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + line * 128 + ((((col & 63) >> 3) ^ (line & 7)) << 4));
+#endif
 }
+// TMA coordinates of a block: (dim0, dim1, dim2)
+#if TC_KV_SLAB
+#define KV_COORD(row) 0, (row), 0
+#else
+#define KV_COORD(row) 0, 0, (row)
+#endif
 
 // Pool row of (page, layer, k|v, head, slot 0) for the 3-D tensor map.
 TC_DEVICE int kv_row(const AttnParams& p, int page, int kv, int head) {
@@ -217,7 +231,7 @@ struct PrefillSmem {
 };
 
 template <int DH, int G>
-__global__ void __launch_bounds__(kPrefillThreads) attn_prefill(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+__global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   constexpr int TPW = 16 / G;  // tokens per warp
   constexpr int TPC = 4 * TPW;
   constexpr int kKeys = kTilePages * kPage;
@@ -244,23 +258,30 @@ __global__ void __launch_bounds__(kPrefillThreads) attn_prefill(const __grid_con
   __syncthreads();
 
   if (warp == 4) {
-    // ---------------- TMA producer: 4 K blocks + 4 V blocks per tile
-    if (lane == 0) {
-      tma_prefetch_desc(&kv_map);
-      for (int t = 0; t < n_tiles; ++t) {
+    // ---------------- TMA producer: 4 K blocks + 4 V blocks per tile. Lanes 0-3 fetch the
+    // next tile's page ids while lane 0 issues the current tile, so block-table latency never
+    // sits between two TMA issues.
+    auto page_id = [&](int gp) { return bt[gp < n_pages ? gp : 0]; };  // beyond the sequence: any page, masked
+    int cur = lane < kTilePages ? page_id(lane) : 0;
+    if (lane == 0) tma_prefetch_desc(&kv_map);
+    for (int t = 0; t < n_tiles; ++t) {
+      int ids[kTilePages];
+#pragma unroll
+      for (int pg = 0; pg < kTilePages; ++pg) ids[pg] = __shfl_sync(0xffffffffu, cur, pg);
+      if (lane < kTilePages && t + 1 < n_tiles) cur = page_id((t + 1) * kTilePages + lane);
+      if (lane == 0) {
         const int st = t % kPrefillStages;
         mbar_wait(&empty_bar[st], ((t / kPrefillStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&full_bar[st], PrefillSmem<DH>::kStageBytes);
         const uint32_t dst = sbase + st * PrefillSmem<DH>::kStageBytes;
 #pragma unroll
         for (int pg = 0; pg < kTilePages; ++pg) {
-          const int gp = t * kTilePages + pg;
-          const int page = bt[gp < n_pages ? gp : 0];  // beyond the sequence: any valid page, masked
-          tma_load_3d(dst + pg * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, kv_row(p, page, 0, kvh), 0);
-          tma_load_3d(dst + (kTilePages + pg) * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], 0, kv_row(p, page, 1, kvh),
-                      0);
+          tma_load_3d(dst + pg * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], KV_COORD(kv_row(p, ids[pg], 0, kvh)));
+          tma_load_3d(dst + (kTilePages + pg) * KvBlock<DH>::kBytes, &kv_map, &full_bar[st],
+                      KV_COORD(kv_row(p, ids[pg], 1, kvh)));
         }
       }
+      __syncwarp();
     }
     return;
   }
@@ -325,7 +346,7 @@ struct DecodeSmem {
 };
 
 template <int DH, int G>
-__global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+__global__ void __launch_bounds__(kDecodeWarps * 32, 2) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   extern __shared__ uint8_t attn_smem_raw[];
   __shared__ uint64_t bars[kDecodeWarps][kDecodeStages];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -340,38 +361,52 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_co
   const int n_warps = gridDim.x * kDecodeWarps;
   const int gw = blockIdx.x * kDecodeWarps + warp;
 
-  // load cursor (lane 0): walks this warp's (item, page) stream S-1 pages ahead
+  // load cursor (lane 0): walks this warp's (item, page) stream S-1 pages ahead. The page id
+  // of the NEXT load is fetched right after an issue, so its latency overlaps a whole page of
+  // compute instead of sitting in front of the TMA.
   int l_item = gw, l_page = -1, issued = 0;
-  auto issue_next = [&]() {
+  int4 l_it = make_int4(0, 0, 0, 0);  // cached current item of the load cursor
+  int nx_kvh = 0, nx_page = -1;        // prefetched next (kv head, page id)
+  auto advance = [&]() {  // move the cursor to the next (item, page) and start fetching its id
     while (l_item < p.n_items) {
-      const int4 it = p.dec_items[l_item];
-      if (l_page < 0) l_page = it.z;
-      if (l_page < it.w) {
-        const int page = p.block_tables[p.seq_bt_off[it.x] + l_page];
-        const int kvh = it.y & 0xff;
-        const int st = issued % kDecodeStages;
-        const uint32_t dst = wbase + st * DecodeSmem<DH>::kStageBytes;
-        fence_proxy_async();
-        mbar_arrive_expect_tx(&full[st], DecodeSmem<DH>::kStageBytes);
-        tma_load_3d(dst, &kv_map, &full[st], 0, kv_row(p, page, 0, kvh), 0);
-        tma_load_3d(dst + KvBlock<DH>::kBytes, &kv_map, &full[st], 0, kv_row(p, page, 1, kvh), 0);
-        ++issued;
+      if (l_page < 0) {
+        l_it = p.dec_items[l_item];
+        l_page = l_it.z;
+      }
+      if (l_page < l_it.w) {
+        nx_kvh = l_it.y & 0xff;
+        nx_page = p.block_tables[l_it.x + l_page];
         ++l_page;
         return;
       }
       l_item += n_warps;
       l_page = -1;
     }
+    nx_page = -1;
   };
-  if (lane == 0)
+  auto issue_next = [&]() {
+    if (nx_page < 0) return;
+    const int st = issued % kDecodeStages;
+    const uint32_t dst = wbase + st * DecodeSmem<DH>::kStageBytes;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[st], DecodeSmem<DH>::kStageBytes);
+    tma_load_3d(dst, &kv_map, &full[st], KV_COORD(kv_row(p, nx_page, 0, nx_kvh)));
+    tma_load_3d(dst + KvBlock<DH>::kBytes, &kv_map, &full[st], KV_COORD(kv_row(p, nx_page, 1, nx_kvh)));
+    ++issued;
+    advance();
+  };
+  if (lane == 0) {
+    advance();
     for (int k = 0; k < kDecodeStages - 1; ++k) issue_next();
+  }
 
   const int r_lo = lane / 4, r_hi = lane / 4 + 8;
   const bool ok_lo = r_lo < G, ok_hi = r_hi < G;
   int n = 0;  // pages consumed by this warp
   for (int item = gw; item < p.n_items; item += n_warps) {
     const int4 it = p.dec_items[item];
-    const int seq = it.x, kvh = it.y & 0xff, d = it.y >> 8;
+    const int kvh = it.y & 0xff, d = it.y >> 8;
+    const int seq = p.dec_seq[d];
     const int chunks = p.dec_chunks[d];
     const int q_row = p.seq_q_start[seq];
     const int kv_len = p.seq_pos0[seq] + 1;
@@ -424,23 +459,72 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) attn_decode(const __grid_co
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) continue;
     __threadfence();
-    // last arriver: merge the request's chunks for this kv head (lane -> DH/32 dims of all G rows)
+    // last arriver: merge the request's chunks (<= 32, host-guaranteed) for this kv head.
+    // lane j loads (m, l) of chunk j for all G rows in one round trip; the per-row max and the
+    // chunk weights go through shuffles; then every lane accumulates DH/32 dims of all G rows,
+    // two chunks of vector loads in flight at a time.
     const int base = p.dec_item_base[d] + kvh * chunks;
+    float wj[G];  // lane j: weight of chunk j for row r (before normalisation)
+    float mj[G], lj[G];
+#pragma unroll
     for (int r = 0; r < G; ++r) {
-      float mm = -INFINITY;
-      for (int j = 0; j < chunks; ++j) mm = fmaxf(mm, __ldcg(p.ws_ml + ((long long)(base + j) * G + r) * 2));
-      float acc[DH / 32] = {}, ll = 0.f;
-      for (int j = 0; j < chunks; ++j) {
-        const long long slot = (long long)(base + j) * G + r;
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + slot * 2));
-        const float f = mm == -INFINITY ? 0.f : exp2f(ml.x - mm);
-        ll += f * ml.y;
+      const float2 ml = lane < chunks ? __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(base + lane) * G + r) * 2))
+                                      : make_float2(-INFINITY, 0.f);
+      mj[r] = ml.x;
+      lj[r] = ml.y;
+    }
+    float inv_l[G];
 #pragma unroll
-        for (int e = 0; e < DH / 32; ++e) acc[e] += f * __ldcg(p.ws_o + slot * DH + e * 32 + lane);
+    for (int r = 0; r < G; ++r) {
+      const float mm = warp_max(mj[r]);
+      wj[r] = (mj[r] == -INFINITY || mm == -INFINITY) ? 0.f : exp2f(mj[r] - mm);
+      const float ll = warp_sum(wj[r] * lj[r]);
+      inv_l[r] = ll > 0.f ? 1.f / ll : 0.f;
+    }
+    constexpr int V = DH / 32;  // dims per lane
+    float acc[G][V];
+#pragma unroll
+    for (int r = 0; r < G; ++r)
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[r][e] = 0.f;
+    for (int j = 0; j < chunks; j += 2) {
+      float oa[2][G][V];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+          const int jj = min(j + u, chunks - 1);
+          const float* src = p.ws_o + ((long long)(base + jj) * G + r) * DH + lane * V;
+          if constexpr (V == 4) {
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+            oa[u][r][0] = t.x; oa[u][r][1] = t.y; oa[u][r][2] = t.z; oa[u][r][3] = t.w;
+          } else {
+            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+            oa[u][r][0] = t.x; oa[u][r][1] = t.y;
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (j + u >= chunks) break;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+          const float f = __shfl_sync(0xffffffffu, wj[r], j + u);
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[r][e] += f * oa[u][r][e];
+        }
       }
-      const float inv = ll > 0.f ? 1.f / ll : 0.f;
+    }
 #pragma unroll
-      for (int e = 0; e < DH / 32; ++e) out_row[r * DH + e * 32 + lane] = __float2bfloat16(acc[e] * inv);
+    for (int r = 0; r < G; ++r) {
+      __nv_bfloat16* dst = out_row + r * DH + lane * V;
+      if constexpr (V == 4) {
+        uint2 w;
+        w.x = pack_bf16(acc[r][0] * inv_l[r], acc[r][1] * inv_l[r]);
+        w.y = pack_bf16(acc[r][2] * inv_l[r], acc[r][3] * inv_l[r]);
+        *reinterpret_cast<uint2*>(dst) = w;
+      } else {
+        *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc[r][0] * inv_l[r], acc[r][1] * inv_l[r]);
+      }
     }
   }
 }

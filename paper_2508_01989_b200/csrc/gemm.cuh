@@ -62,7 +62,7 @@ struct QkvRopeArgs {
 
 constexpr int kGemmBM = 128;
 #ifndef TC_GEMM_BK
-#define TC_GEMM_BK 32
+#define TC_GEMM_BK 64
 #endif
 constexpr int kGemmBK = TC_GEMM_BK;  // K per pipeline stage (32 or 64 bf16 = 64 / 128 B rows)
 constexpr int kGemmThreads = 256;

@@ -129,8 +129,11 @@ void init_kernel_attrs(int dev) {
   DeviceGuard g(dev);
   set_gemm_smem<128, 0>(); set_gemm_smem<128, 1>(); set_gemm_smem<128, 2>(); set_gemm_smem<128, 3>(); set_gemm_smem<128, 4>(); set_gemm_smem<128, 5>();
   set_gemm_smem<256, 0>(); set_gemm_smem<256, 1>(); set_gemm_smem<256, 2>(); set_gemm_smem<256, 3>(); set_gemm_smem<256, 4>(); set_gemm_smem<256, 5>();
+  // attention kernels run 2 CTAs/SM (~97 KB each): ask for the maximum shared-memory carveout,
+  // otherwise the driver's default split leaves room for only one (ncu: occupancy 7.8%)
   auto attr = [](const void* fn, int bytes) {
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   };
   attr((const void*)tc::attn_prefill<64, 2>, tc::PrefillSmem<64>::kBytes);
   attr((const void*)tc::attn_prefill<128, 4>, tc::PrefillSmem<128>::kBytes);
@@ -633,6 +636,9 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     for (int i = 0; i < n_dec; ++i) n += (long long)m.n_kv_heads * ((st->decode[i].pos / ps + 1 + per - 1) / per);
     return n;
   };
+  int max_pages = 1;
+  for (int i = 0; i < n_dec; ++i) max_pages = std::max(max_pages, st->decode[i].pos / ps + 1);
+  ppi = std::max(ppi, (max_pages + 31) / 32);  // <= 32 items per (request, kv head): one merge round trip
   while (count_items(ppi) > kMaxDecodeItems) ppi *= 2;
   const int n_items = (int)count_items(ppi);
   // layout of the metadata block
@@ -703,7 +709,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       for (int kh = 0; kh < m.n_kv_heads; ++kh)
         for (int c = 0; c < chunks; ++c) {
           int32_t* e = h + o_items + 4 * (size_t)it++;
-          e[0] = n_pf + j;
+          e[0] = h[o_bo + n_pf + j];  // block-table offset of the request
           e[1] = kh | (j << 8);
           e[2] = c * ppi;
           e[3] = std::min(pages, (c + 1) * ppi);
@@ -1003,9 +1009,15 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
       TC_REQUIRE(rows < (1ull << 31), "create: KV pool too large for 32-bit TMA row coordinates");
       // dims {64 dims, pool rows, head_dim/64 halves}: each half of a 16-row block lands as a
       // separate 16-line 128 B-swizzled slab (bank-conflict-free ldmatrix, K-major SW128 layout)
+#if TC_KV_SLAB
       const cuuint64_t dims[3] = {64, rows, (cuuint64_t)(m.head_dim / 64)};
       const cuuint64_t strides[2] = {(cuuint64_t)m.head_dim * 2, 128};
       const cuuint32_t box[3] = {64, (cuuint32_t)desc->page_size, (cuuint32_t)(m.head_dim / 64)};
+#else
+      const cuuint64_t dims[3] = {64, (cuuint64_t)(m.head_dim / 64), rows};
+      const cuuint64_t strides[2] = {128, (cuuint64_t)m.head_dim * 2};
+      const cuuint32_t box[3] = {64, (cuuint32_t)(m.head_dim / 64), (cuuint32_t)desc->page_size};
+#endif
       const cuuint32_t estr[3] = {1, 1, 1};
       const CUresult r = tensor_map_encoder()(&I->kv_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, I->kv, dims, strides, box,
                                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

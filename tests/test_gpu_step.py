@@ -240,7 +240,7 @@ def test_llama_shape_mixed_step(llama_l2):
 def test_qwen_shape_bias_and_group5():
     """Qwen2.5-14B layer shapes (2 layers, vocab 152064): QKV bias, GQA group 5 (40 q / 8 kv heads)."""
     from paper_2508_01989_b200 import Instance
-    with Instance("qwen2_5_14b:L2", weight_seed=5, kv_pool_tokens=1 << 14, max_step_tokens=1024, max_seqs=32,
+    with Instance("qwen2_5_14b:L2", weight_seed=5, kv_pool_tokens=1 << 14, max_step_tokens=2048, max_seqs=32,
                   max_context=4096) as inst:
         d = mr.preset("qwen2_5_14b:L2")
         model = mr.RefModel(d, mr.weights_from_device(inst, d), max_pos=4096)

@@ -43,8 +43,22 @@ def main():
             except Exception as ex:  # noqa: BLE001
                 us = str(ex)[:60]
             res[f"bn{bn}_s{sp}"] = us
+        # same-box comparison point (NOT our path): cuBLAS via torch.matmul on the same operands
+        try:
+            for _ in range(3):
+                torch.matmul(a, b.t())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                torch.matmul(a, b.t())
+            e1.record()
+            torch.cuda.synchronize()
+            res["cublas_bf16"] = e0.elapsed_time(e1) / 20 * 1e3
+        except Exception as ex:  # noqa: BLE001
+            res["cublas_bf16"] = str(ex)[:60]
         flops = 2.0 * m * n * k
-        best = min((v for v in res.values() if isinstance(v, float)), default=None)
+        best = min((v for kk, v in res.items() if isinstance(v, float) and kk != "cublas_bf16"), default=None)
         out[name] = {"M": m, "N": n, "K": k, "us": res, "best_tflops": flops / best / 1e6 if best else None}
         print(name, {k: (round(v, 1) if isinstance(v, float) else v) for k, v in res.items()},
               "best TF/s %.0f" % (flops / best / 1e6), flush=True)
