@@ -336,6 +336,9 @@ __global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_
 
 // ============================================================== decode
 constexpr int kDecodeStages = 3;
+#ifndef TC_DECODE_FUSED_MERGE
+#define TC_DECODE_FUSED_MERGE 1  // 1: last-arriving warp merges split items; 0: attn_decode_combine kernel
+#endif
 constexpr int kDecodeWarps = 4;
 
 template <int DH>
@@ -449,6 +452,9 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 2) attn_decode(const __grid
       for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(wo + c * 8) = make_float2(o[c][0], o[c][1]);
       if (lane % 4 == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)item * G + r_lo) * 2) = make_float2(m[0], l[0]);
     }
+#if !TC_DECODE_FUSED_MERGE
+    continue;  // merged by attn_decode_combine
+#endif
     __threadfence();
     __syncwarp();
     int last = 0;
@@ -527,6 +533,51 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 2) attn_decode(const __grid
       }
     }
   }
+}
+
+// Separate merge of split decode items (TC_DECODE_FUSED_MERGE = 0): one warp per (request,
+// kv head), same vectorised merge as the fused path.
+template <int DH, int G>
+__global__ void attn_decode_combine(AttnParams p, int n_dec) {
+  const int lane = threadIdx.x % 32;
+  const int wid = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (wid >= n_dec * p.n_kv_heads) return;
+  const int d = wid / p.n_kv_heads, kvh = wid % p.n_kv_heads;
+  const int chunks = p.dec_chunks[d];
+  if (chunks <= 1) return;
+  const int base = p.dec_item_base[d] + kvh * chunks;
+  const int q_row = p.seq_q_start[p.dec_seq[d]];
+  __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
+  float wj[G], mj[G], lj[G], inv_l[G];
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+    const float2 ml = lane < chunks ? __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(base + lane) * G + r) * 2))
+                                    : make_float2(-INFINITY, 0.f);
+    mj[r] = ml.x;
+    lj[r] = ml.y;
+  }
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+    const float mm = warp_max(mj[r]);
+    wj[r] = (mj[r] == -INFINITY || mm == -INFINITY) ? 0.f : exp2f(mj[r] - mm);
+    const float ll = warp_sum(wj[r] * lj[r]);
+    inv_l[r] = ll > 0.f ? 1.f / ll : 0.f;
+  }
+  constexpr int V = DH / 32;
+  float acc[G][V] = {};
+  for (int j = 0; j < chunks; ++j) {
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      const float f = __shfl_sync(0xffffffffu, wj[r], j);
+      const float* src = p.ws_o + ((long long)(base + j) * G + r) * DH + lane * V;
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[r][e] += f * __ldcg(src + e);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < G; ++r)
+#pragma unroll
+    for (int e = 0; e < V; ++e) out_row[r * DH + lane * V + e] = __float2bfloat16(acc[r][e] * inv_l[r]);
 }
 
 }  // namespace tc

@@ -131,6 +131,12 @@ void init_kernel_attrs(int dev) {
   set_gemm_smem<256, 0>(); set_gemm_smem<256, 1>(); set_gemm_smem<256, 2>(); set_gemm_smem<256, 3>(); set_gemm_smem<256, 4>(); set_gemm_smem<256, 5>();
   // attention kernels run 2 CTAs/SM (~97 KB each): ask for the maximum shared-memory carveout,
   // otherwise the driver's default split leaves room for only one (ncu: occupancy 7.8%)
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
   auto attr = [](const void* fn, int bytes) {
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
@@ -248,6 +254,23 @@ struct SkWorkspace {
   int* cnt = nullptr;
 };
 
+// 2-SM (CTA pair) GEMM: 256 x 256 tiles, tcgen05.mma.cta_group::2. Used for M > kGemm2MinM.
+constexpr int kGemm2MinM = 1 << 30;  // set after measurement (tools/gemm_bench.py, bn = 512 forces it)
+
+void launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb128, const tc::GemmArgs& args, int epi, int grid,
+                     cudaStream_t s) {
+  const int smem = tc::Gemm2Cfg::kSmemBytes;
+  switch (epi) {
+    case tc::EPI_BF16: tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    case tc::EPI_BF16_BIAS: tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    case tc::EPI_RESID_F32: tc::gemm_bf16_tcgen05_2sm<tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    case tc::EPI_SWIGLU: tc::gemm_bf16_tcgen05_2sm<tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    case tc::EPI_F32: tc::gemm_bf16_tcgen05_2sm<tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    case tc::EPI_QKV_ROPE: tc::gemm_bf16_tcgen05_2sm<tc::EPI_QKV_ROPE><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
+  }
+}
+
 // out = epi(A[M,K] * W[N,K]^T). a_map: box 128 rows over the activation buffer.
 int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
              int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
@@ -255,8 +278,53 @@ int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo,
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(K % 64 == 0, "gemm: K must be a multiple of 64");
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
-  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256, "gemm: tile width must be 128 or 256");
-  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits, red_out != nullptr);
+  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256 || force_bn == 512,
+             "gemm: tile width must be 128, 256 or 512 (= 2-SM 256 x 256)");
+  const bool two_sm = N % 256 == 0 && (force_bn == 512 || (force_bn == 0 && M > kGemm2MinM));
+  if (two_sm) {
+    // pair tiles of 256 rows; splits only through red.add (residual / streaming epilogues)
+    tc::GemmArgs args{};
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.m_tiles = (M + 255) / 256;
+    args.n_tiles = N / 256;
+    args.kb = K / tc::kGemmBK;
+    const long long tiles = (long long)args.m_tiles * args.n_tiles;
+    const int pairs = sms / 2;
+    int sp = 1;
+    if (force_splits > 0 && (epi == tc::EPI_RESID_F32 || red_out)) {
+      sp = force_splits;
+    } else if ((epi == tc::EPI_RESID_F32 || red_out) && tiles < pairs) {
+      double best = 1e30;
+      for (int cand = 1; cand <= std::min(16, std::max(1, args.kb / 4)); ++cand) {
+        const long long waves = (tiles * cand + pairs - 1) / pairs;
+        const double t = (double)waves * ((args.kb + cand - 1) / cand + 8);
+        if (t < best - 1e-9) {
+          best = t;
+          sp = cand;
+        }
+      }
+    }
+    args.splits = sp;
+    args.units = (int)(tiles * sp);
+    args.out = out;
+    args.ldo = ldo;
+    args.bias = bias;
+    args.ws = sk.ws;
+    args.tile_cnt = sk.cnt;
+    args.red_out = red_out;
+    if (epi == tc::EPI_QKV_ROPE && red_out == nullptr) {
+      TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
+      TC_REQUIRE(256 % rope->head_dim == 0, "gemm: tile width must cover whole heads");
+      args.rope = *rope;
+    }
+    const int grid = 2 * (int)std::min<long long>(pairs, args.units);
+    launch_gemm_2sm(a_map, w.map(128), args, epi, grid, s);
+    TC_CUDA(cudaGetLastError());
+    return 1;
+  }
+  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn == 512 ? 0 : force_bn, force_splits, red_out != nullptr);
   TC_REQUIRE((long long)c.m_tiles * c.n_tiles <= kSkMaxTiles, "gemm: too many tiles");
   tc::GemmArgs args{};
   args.M = M;
@@ -580,7 +648,15 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
   if (n_dec > 0) {
     tc::attn_decode<DH, G><<<dec_grid, tc::kDecodeWarps * 32, tc::DecodeSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
     ++I->launches;
+#if TC_DECODE_FUSED_MERGE
     (void)combine;  // split requests are merged inside attn_decode (last arriver)
+#else
+    if (combine) {
+      const int warps = n_dec * hk;
+      tc::attn_decode_combine<DH, G><<<(warps + 3) / 4, 128, 0, I->stream>>>(p, n_dec);
+      ++I->launches;
+    }
+#endif
   }
   TC_CUDA(cudaGetLastError());
 }

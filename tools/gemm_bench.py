@@ -15,7 +15,7 @@ SHAPES = {  # name: (M, N, K, epilogue)
     "qkv_d64": (64, 6144, 4096, 0), "o_d64": (64, 4096, 4096, 2), "gate_up_d64": (64, 28672, 4096, 3),
     "down_d64": (64, 4096, 14336, 2), "gate_up_1100": (1100, 28672, 4096, 3),
 }
-VARIANTS = [(0, 0), (256, 1), (128, 1), (256, 3), (256, 5), (256, 7), (256, 9), (128, 3)]
+VARIANTS = [(0, 0), (256, 1), (256, 3), (256, 5), (128, 3), (512, 0), (512, 1), (512, 3)]
 
 
 def main():
