@@ -1,26 +1,24 @@
 // Paged attention for the hybrid step (SURVEY.md 2, K1 + K2).
 //
 // KV pool layout (page-major so one request's KV migrates as whole pages):
-//   pool[page][layer][k|v][kv_head][slot 0..PS-1][head_dim]   (bf16, PS = 16)
-// One (page, layer, k|v, kv_head) block is 16 rows x head_dim, 4 KiB contiguous for
-// head_dim 128. It is fetched by ONE TMA instruction through a 3-D tensor map
-// {64 dims, pool rows, head_dim/64 halves} (strides 256 B, 128 B) with 128 B swizzle:
-// each 64-dim half lands as its own 16-line slab (the K-major SW128 layout), so the
-// 8 keys of an ldmatrix phase hit 8 distinct bank groups
-// (address = half*2048 + key*128 + ((chunk ^ key) & 7) * 16). Completion is tracked with mbarrier transaction
-// counts, so no thread computes per-chunk gather addresses.
+//   pool[page][layer][kv_head][k|v][slot 0..PS-1][head_dim]   (bf16, PS = 16)
+// The K block and the V block of one (page, layer, kv_head) are adjacent: 32 rows x head_dim,
+// 8 KiB contiguous at head_dim 128, fetched by ONE TMA instruction through a 3-D tensor map
+// {64 dims, pool rows, head_dim/64 halves} (strides 256 B, 128 B) with 128 B swizzle: each
+// 64-dim half lands as its own 32-line slab (K rows 0-15, V rows 16-31; the K-major SW128
+// layout), so the 8 keys of an ldmatrix phase hit 8 distinct bank groups
+// (address = half*4096 + row*128 + ((chunk ^ row) & 7) * 16). Completion is tracked with
+// mbarrier transaction counts, so no thread computes per-chunk gather addresses.
 //
 //  * attn_prefill  -- chunked-prefill queries (a chunk may span prompts; each slice
 //    is a sequence) attend causally to the paged prefix + in-chunk keys. CTA =
 //    (16/G tokens x G heads) x 4 consumer warps of one GQA group + 1 TMA producer
 //    warp; 64-key tiles (4 pages) in a 3-stage full/empty mbarrier ring. QK^T and
 //    PV on tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate), online softmax.
-//  * attn_decode   -- split-KV at warp granularity: a work item is (request,
-//    kv_head, run of pages); a persistent grid of independent warps walks its
-//    items with a private 4-stage page ring (each warp issues its own TMA loads
-//    S-1 pages ahead, across item boundaries). For requests split into several items
-//    the warp that finishes an item LAST (atomic counter per request and kv head)
-//    merges the partials -- no separate combine launch, no waiting.
+//  * attn_decode   -- balanced page stream: every SM gets the same number of page-heads
+//    (contiguous range over all (request, kv head) segments); a producer warp streams
+//    K/V pages through a 24-stage TMA ring, 4 consumer warps split the pages and merge
+//    in shared memory; only segments cut by a CTA boundary merge through global memory.
 #pragma once
 
 #include "common.cuh"
@@ -39,14 +37,14 @@ struct AttnParams {
   const int* block_tables;   // flat page ids
   const int* qblk_seq;       // prefill work list
   const int* qblk_off;
-  const int4* dec_items;     // decode work: (block-table offset, kvh | decode index << 8, page0, page1)
-  int n_items;
-  const int* dec_seq;        // decode index -> sequence
-  const int* dec_item_base;  // decode index -> first item; items (d, kvh, j) at base + kvh * chunks + j
-  const int* dec_chunks;     // decode index -> items per kv head
-  float* ws_o;               // [item][G][DH]
-  float* ws_ml;              // [item][G][2]
-  int* dec_cnt;              // [decode][kv head] arrival counters (zero; the last arriver resets)
+  // decode work (see attn_decode): segments = (decode request, kv head)
+  const int4* dec_seg_a;     // [seg] (block-table offset, kv_len, q row, kv head)
+  const int4* dec_seg_b;     // [seg] (parts = CTAs covering the segment, first ws slot, 0, 0)
+  const int4* dec_entries;   // per-CTA entry lists: (seg, page0, page1, part)
+  const int* dec_cta_off;    // [grid + 1] entry offsets
+  float* ws_o;               // [slot][G][DH] partial o of segments cut by CTA boundaries
+  float* ws_ml;              // [slot][G][2]
+  int* dec_cnt;              // [seg] arrival counters (zero; the last arriver resets)
 };
 
 TC_DEVICE void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -79,34 +77,24 @@ constexpr int kPage = 16;  // tokens per KV page (tc_instance_desc.page_size)
 template <int DH>
 struct KvBlock {
   static constexpr int kBytes = kPage * DH * 2;  // one (page, k|v, head) block
+  static constexpr int kPairBytes = 2 * kBytes;  // K block + V block: one TMA box
   static constexpr int kHalves = DH / 64;
 };
 
-#ifndef TC_KV_SLAB
-#define TC_KV_SLAB 1  // 1: {64, rows, halves} box (one slab per half); 0: {64, halves, rows} (interleaved)
-#endif
-// Swizzled smem address of (key, col) inside consecutive page blocks starting at base.
+// Swizzled smem address of (key, col) of K (v = 0) or V (v = 1) inside consecutive page pairs
+// starting at base.
 template <int DH>
-TC_DEVICE uint32_t kv_addr(uint32_t base, int key, int col) {
-  const int row = key & (kPage - 1);
-#if TC_KV_SLAB
-  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + (col >> 6) * (kPage * 128) + row * 128 +
+TC_DEVICE uint32_t kv_addr(uint32_t base, int key, int col, int v) {
+  const int row = (key & (kPage - 1)) + v * kPage;
+  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kPairBytes + (col >> 6) * (2 * kPage * 128) + row * 128 +
                            ((((col & 63) >> 3) ^ (row & 7)) << 4));
-#else
-  const int line = row * KvBlock<DH>::kHalves + (col >> 6);
-  return base + (uint32_t)((key >> 4) * KvBlock<DH>::kBytes + line * 128 + ((((col & 63) >> 3) ^ (line & 7)) << 4));
-#endif
 }
-// TMA coordinates of a block: (dim0, dim1, dim2)
-#if TC_KV_SLAB
+// TMA coordinates (dim0, dim1, dim2) of the K/V pair starting at pool row `row`
 #define KV_COORD(row) 0, (row), 0
-#else
-#define KV_COORD(row) 0, 0, (row)
-#endif
 
-// Pool row of (page, layer, k|v, head, slot 0) for the 3-D tensor map.
-TC_DEVICE int kv_row(const AttnParams& p, int page, int kv, int head) {
-  return (((page * p.n_layers + p.layer) * 2 + kv) * p.n_kv_heads + head) * kPage;
+// Pool row of (page, layer, head, K, slot 0) for the 3-D tensor map.
+TC_DEVICE int kv_row(const AttnParams& p, int page, int head) {
+  return (((page * p.n_layers + p.layer) * p.n_kv_heads + head) * 2) * kPage;
 }
 
 // Q fragment (A operand) of 16 rows: rows lo / hi -> (token, head).
@@ -138,7 +126,7 @@ TC_DEVICE void attn_qk(const uint32_t (&qf)[DH / 16][4], uint32_t k_smem, int kb
 #pragma unroll
     for (int t = 0; t < NT; t += 2) {
       uint32_t b0, b1, b2, b3;
-      ldsm_x4(kv_addr<DH>(k_smem, kbase + t * 8 + (j / 2) * 8 + r, ks * 16 + (j % 2) * 8), b0, b1, b2, b3);
+      ldsm_x4(kv_addr<DH>(k_smem, kbase + t * 8 + (j / 2) * 8 + r, ks * 16 + (j % 2) * 8, 0), b0, b1, b2, b3);
       mma_bf16_16816(s[t], qf[ks], b0, b1);
       mma_bf16_16816(s[t + 1], qf[ks], b2, b3);
     }
@@ -160,7 +148,7 @@ TC_DEVICE void attn_pv(const float (&pr)[NT][4], uint32_t v_smem, int kbase, flo
 #pragma unroll
     for (int n = 0; n < DH / 8; n += 2) {
       uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(kv_addr<DH>(v_smem, kbase + kk * 16 + (j % 2) * 8 + r, n * 8 + (j / 2) * 8), b0, b1, b2, b3);
+      ldsm_x4_t(kv_addr<DH>(v_smem, kbase + kk * 16 + (j % 2) * 8 + r, n * 8 + (j / 2) * 8, 1), b0, b1, b2, b3);
       mma_bf16_16816(o[n], a, b0, b1);
       mma_bf16_16816(o[n + 1], a, b2, b3);
     }
@@ -226,7 +214,7 @@ constexpr int kTilePages = 4;         // 64 keys per tile
 
 template <int DH>
 struct PrefillSmem {
-  static constexpr int kStageBytes = 2 * kTilePages * KvBlock<DH>::kBytes;  // K pages then V pages
+  static constexpr int kStageBytes = kTilePages * KvBlock<DH>::kPairBytes;  // 4 (K, V) page pairs
   static constexpr int kBytes = kPrefillStages * kStageBytes + 1024;
 };
 
@@ -276,9 +264,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_
         const uint32_t dst = sbase + st * PrefillSmem<DH>::kStageBytes;
 #pragma unroll
         for (int pg = 0; pg < kTilePages; ++pg) {
-          tma_load_3d(dst + pg * KvBlock<DH>::kBytes, &kv_map, &full_bar[st], KV_COORD(kv_row(p, ids[pg], 0, kvh)));
-          tma_load_3d(dst + (kTilePages + pg) * KvBlock<DH>::kBytes, &kv_map, &full_bar[st],
-                      KV_COORD(kv_row(p, ids[pg], 1, kvh)));
+          tma_load_3d(dst + pg * KvBlock<DH>::kPairBytes, &kv_map, &full_bar[st], KV_COORD(kv_row(p, ids[pg], kvh)));
         }
       }
       __syncwarp();
@@ -306,7 +292,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_
     const int st = t % kPrefillStages;
     mbar_wait(&full_bar[st], (t / kPrefillStages) & 1);
     const uint32_t k_smem = sbase + st * PrefillSmem<DH>::kStageBytes;
-    const uint32_t v_smem = k_smem + kTilePages * KvBlock<DH>::kBytes;
+    const uint32_t v_smem = k_smem;  // kv_addr selects the V rows
     float s[8][4];
     attn_qk<DH, 8>(qf, k_smem, 0, s);
     attn_softmax_step<DH, 8>(s, t * kKeys, lim_lo, lim_hi, p.scale_log2, m, l, o);
@@ -335,249 +321,288 @@ __global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_
 }
 
 // ============================================================== decode
-constexpr int kDecodeStages = 3;
-#ifndef TC_DECODE_FUSED_MERGE
-#define TC_DECODE_FUSED_MERGE 1  // 1: last-arriving warp merges split items; 0: attn_decode_combine kernel
-#endif
-constexpr int kDecodeWarps = 4;
-
-template <int DH>
-struct DecodeSmem {
-  static constexpr int kStageBytes = 2 * KvBlock<DH>::kBytes;  // one page: K block then V block
-  static constexpr int kWarpBytes = kDecodeStages * kStageBytes;
-  static constexpr int kBytes = kDecodeWarps * kWarpBytes + 1024;
-};
+// Work decomposition (host, step_launch): a SEGMENT is (decode request, kv head) and covers
+// that request's KV pages 0..ceil(kv_len/16)-1. All segments' pages, laid end to end, form one
+// page stream of W page-heads; CTA c (one per SM, persistent) takes the contiguous range
+// [W*c/NC, W*(c+1)/NC), so every SM streams the same number of bytes whatever the context
+// mix. A CTA's range is a list of ENTRIES (segment, page0, page1, part).
+//
+// Inside a CTA: one producer warp walks the entries and streams each page's K and V blocks
+// (2 TMA loads, 8 KiB at head_dim 128) into a deep ring, plus the segment's q rows (one bulk
+// copy per entry) into a double-buffered q slot; it never waits for a consumer except on a
+// full ring. Consumer warp w takes ring stages w, w+4, w+8, ... and keeps its own online-
+// softmax state per entry; at the end of an entry the 4 partial states meet in shared memory
+// (one named barrier) and warp (entry % 4) merges them. Only segments cut by a CTA boundary
+// (at most 2 per CTA) go through global memory: the merging warp writes its partial, and the
+// CTA that arrives last on the segment's counter combines the parts.
+constexpr int kDecConsumers = 4;
+constexpr int kDecThreads = (kDecConsumers + 1) * 32;
+constexpr int kDecRingBytes = 192 * 1024;
 
 template <int DH, int G>
-__global__ void __launch_bounds__(kDecodeWarps * 32, 2) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  extern __shared__ uint8_t attn_smem_raw[];
-  __shared__ uint64_t bars[kDecodeWarps][kDecodeStages];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t wbase = ((smem_u32(attn_smem_raw) + 1023u) & ~1023u) + warp * DecodeSmem<DH>::kWarpBytes;
-  uint64_t* full = bars[warp];
-  if (lane == 0) {
-    for (int s = 0; s < kDecodeStages; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-    tma_prefetch_desc(&kv_map);
-  }
-  __syncwarp();
-  const int n_warps = gridDim.x * kDecodeWarps;
-  const int gw = blockIdx.x * kDecodeWarps + warp;
+struct DecodeSmem {
+  static constexpr int kStageBytes = KvBlock<DH>::kPairBytes;  // one page-head: K block then V block
+  static constexpr int kStages = kDecRingBytes / kStageBytes;
+  static constexpr int kQBytes = G * DH * 2;
+  static constexpr int kPartFloats = kDecConsumers * G * DH;  // per buffer
+  static constexpr int kOffQ = kDecRingBytes;
+  static constexpr int kOffPart = kOffQ + 2 * ((kQBytes + 127) / 128 * 128);
+  static constexpr int kOffMl = kOffPart + 2 * kPartFloats * 4;
+  static constexpr int kBytes = kOffMl + 2 * kDecConsumers * G * 2 * 4 + 1024;
+  // Stage g is consumed by warp g % 4. With S a multiple of 4 every slot has ONE owner warp, which
+  // waits for use k+1 only after finishing use k; otherwise a warp running a lap ahead could pass
+  // a parity wait on a phase that has not landed yet (mbarrier parity ABA).
+  static_assert(kStages % kDecConsumers == 0, "decode ring: stages must be a multiple of the consumer warps");
+  static_assert(kBytes <= 227 * 1024, "decode smem");
+};
 
-  // load cursor (lane 0): walks this warp's (item, page) stream S-1 pages ahead. The page id
-  // of the NEXT load is fetched right after an issue, so its latency overlaps a whole page of
-  // compute instead of sitting in front of the TMA.
-  int l_item = gw, l_page = -1, issued = 0;
-  int4 l_it = make_int4(0, 0, 0, 0);  // cached current item of the load cursor
-  int nx_kvh = 0, nx_page = -1;        // prefetched next (kv head, page id)
-  auto advance = [&]() {  // move the cursor to the next (item, page) and start fetching its id
-    while (l_item < p.n_items) {
-      if (l_page < 0) {
-        l_it = p.dec_items[l_item];
-        l_page = l_it.z;
-      }
-      if (l_page < l_it.w) {
-        nx_kvh = l_it.y & 0xff;
-        nx_page = p.block_tables[l_it.x + l_page];
-        ++l_page;
-        return;
-      }
-      l_item += n_warps;
-      l_page = -1;
-    }
-    nx_page = -1;
-  };
-  auto issue_next = [&]() {
-    if (nx_page < 0) return;
-    const int st = issued % kDecodeStages;
-    const uint32_t dst = wbase + st * DecodeSmem<DH>::kStageBytes;
-    fence_proxy_async();
-    mbar_arrive_expect_tx(&full[st], DecodeSmem<DH>::kStageBytes);
-    tma_load_3d(dst, &kv_map, &full[st], KV_COORD(kv_row(p, nx_page, 0, nx_kvh)));
-    tma_load_3d(dst + KvBlock<DH>::kBytes, &kv_map, &full[st], KV_COORD(kv_row(p, nx_page, 1, nx_kvh)));
-    ++issued;
-    advance();
-  };
-  if (lane == 0) {
-    advance();
-    for (int k = 0; k < kDecodeStages - 1; ++k) issue_next();
-  }
+TC_DEVICE void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+TC_DEVICE void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kDecConsumers * 32) : "memory"); }
 
-  const int r_lo = lane / 4, r_hi = lane / 4 + 8;
-  const bool ok_lo = r_lo < G, ok_hi = r_hi < G;
-  int n = 0;  // pages consumed by this warp
-  for (int item = gw; item < p.n_items; item += n_warps) {
-    const int4 it = p.dec_items[item];
-    const int kvh = it.y & 0xff, d = it.y >> 8;
-    const int seq = p.dec_seq[d];
-    const int chunks = p.dec_chunks[d];
-    const int q_row = p.seq_q_start[seq];
-    const int kv_len = p.seq_pos0[seq] + 1;
-    uint32_t qf[DH / 16][4];
-    attn_load_q<DH>(p, q_row, kvh * G + (ok_lo ? r_lo : 0), ok_lo, q_row, kvh * G + (ok_hi ? r_hi : 0), ok_hi, qf);
-    float o[DH / 8][4];
+// Merge n partial states (m, l in the log2 domain; o unnormalised) for G rows; lane handles
+// dims lane*V .. lane*V+V-1. load_ml(j, r) -> float2(m, l); load_o(j, r, dst[V]).
+template <int DH, int G, typename LoadMl, typename LoadO>
+TC_DEVICE void merge_partials(int n, LoadMl&& load_ml, LoadO&& load_o, float (&acc)[G][DH / 32], float (&mm)[G],
+                              float (&ll)[G]) {
+  constexpr int V = DH / 32;
 #pragma unroll
-    for (int c = 0; c < DH / 8; ++c) o[c][0] = o[c][1] = o[c][2] = o[c][3] = 0.f;
-    float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-    for (int pg = it.z; pg < it.w; ++pg, ++n) {
-      if (lane == 0) issue_next();
-      const int st = n % kDecodeStages;
-      mbar_wait(&full[st], (n / kDecodeStages) & 1);
-      const uint32_t k_smem = wbase + st * DecodeSmem<DH>::kStageBytes;
-      float s[2][4];
-      attn_qk<DH, 2>(qf, k_smem, 0, s);
-      attn_softmax_step<DH, 2>(s, pg * kPage, kv_len, kv_len, p.scale_log2, m, l, o);
-      attn_pv<DH, 2>(s, k_smem + KvBlock<DH>::kBytes, 0, o);
-      __syncwarp();
-    }
+  for (int r = 0; r < G; ++r) {
+    float mx = -INFINITY;
+    for (int j = 0; j < n; ++j) mx = fmaxf(mx, load_ml(j, r).x);
+    mm[r] = mx;
+    ll[r] = 0.f;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      l[h] += __shfl_xor_sync(0xffffffffu, l[h], 1);
-      l[h] += __shfl_xor_sync(0xffffffffu, l[h], 2);
-    }
-    const int c0 = (lane % 4) * 2;
-    __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
-    if (chunks == 1) {
-      if (ok_lo) {  // only rows < G (lanes 0 .. 4G-1) carry results
-        const float inv = 1.f / l[0];
-#pragma unroll
-        for (int c = 0; c < DH / 8; ++c)
-          *reinterpret_cast<uint32_t*>(out_row + r_lo * DH + c * 8 + c0) = pack_bf16(o[c][0] * inv, o[c][1] * inv);
-      }
-      continue;
-    }
-    if (ok_lo) {
-      float* wo = p.ws_o + ((long long)item * G + r_lo) * DH + c0;
-#pragma unroll
-      for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(wo + c * 8) = make_float2(o[c][0], o[c][1]);
-      if (lane % 4 == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)item * G + r_lo) * 2) = make_float2(m[0], l[0]);
-    }
-#if !TC_DECODE_FUSED_MERGE
-    continue;  // merged by attn_decode_combine
-#endif
-    __threadfence();
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      int* cnt = p.dec_cnt + d * p.n_kv_heads + kvh;
-      last = atomicAdd(cnt, 1) == chunks - 1;
-      if (last) *cnt = 0;  // ready for the next layer / step
-    }
-    if (!__shfl_sync(0xffffffffu, last, 0)) continue;
-    __threadfence();
-    // last arriver: merge the request's chunks (<= 32, host-guaranteed) for this kv head.
-    // lane j loads (m, l) of chunk j for all G rows in one round trip; the per-row max and the
-    // chunk weights go through shuffles; then every lane accumulates DH/32 dims of all G rows,
-    // two chunks of vector loads in flight at a time.
-    const int base = p.dec_item_base[d] + kvh * chunks;
-    float wj[G];  // lane j: weight of chunk j for row r (before normalisation)
-    float mj[G], lj[G];
+    for (int e = 0; e < V; ++e) acc[r][e] = 0.f;
+  }
+  for (int j = 0; j < n; ++j) {
 #pragma unroll
     for (int r = 0; r < G; ++r) {
-      const float2 ml = lane < chunks ? __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(base + lane) * G + r) * 2))
-                                      : make_float2(-INFINITY, 0.f);
-      mj[r] = ml.x;
-      lj[r] = ml.y;
-    }
-    float inv_l[G];
+      const float2 ml = load_ml(j, r);
+      const float w = ml.x == -INFINITY ? 0.f : exp2f(ml.x - mm[r]);
+      ll[r] += w * ml.y;
+      float o[V];
+      load_o(j, r, o);
 #pragma unroll
-    for (int r = 0; r < G; ++r) {
-      const float mm = warp_max(mj[r]);
-      wj[r] = (mj[r] == -INFINITY || mm == -INFINITY) ? 0.f : exp2f(mj[r] - mm);
-      const float ll = warp_sum(wj[r] * lj[r]);
-      inv_l[r] = ll > 0.f ? 1.f / ll : 0.f;
-    }
-    constexpr int V = DH / 32;  // dims per lane
-    float acc[G][V];
-#pragma unroll
-    for (int r = 0; r < G; ++r)
-#pragma unroll
-      for (int e = 0; e < V; ++e) acc[r][e] = 0.f;
-    for (int j = 0; j < chunks; j += 2) {
-      float oa[2][G][V];
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int r = 0; r < G; ++r) {
-          const int jj = min(j + u, chunks - 1);
-          const float* src = p.ws_o + ((long long)(base + jj) * G + r) * DH + lane * V;
-          if constexpr (V == 4) {
-            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
-            oa[u][r][0] = t.x; oa[u][r][1] = t.y; oa[u][r][2] = t.z; oa[u][r][3] = t.w;
-          } else {
-            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
-            oa[u][r][0] = t.x; oa[u][r][1] = t.y;
-          }
-        }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (j + u >= chunks) break;
-#pragma unroll
-        for (int r = 0; r < G; ++r) {
-          const float f = __shfl_sync(0xffffffffu, wj[r], j + u);
-#pragma unroll
-          for (int e = 0; e < V; ++e) acc[r][e] += f * oa[u][r][e];
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-      __nv_bfloat16* dst = out_row + r * DH + lane * V;
-      if constexpr (V == 4) {
-        uint2 w;
-        w.x = pack_bf16(acc[r][0] * inv_l[r], acc[r][1] * inv_l[r]);
-        w.y = pack_bf16(acc[r][2] * inv_l[r], acc[r][3] * inv_l[r]);
-        *reinterpret_cast<uint2*>(dst) = w;
-      } else {
-        *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc[r][0] * inv_l[r], acc[r][1] * inv_l[r]);
-      }
+      for (int e = 0; e < V; ++e) acc[r][e] += w * o[e];
     }
   }
 }
 
-// Separate merge of split decode items (TC_DECODE_FUSED_MERGE = 0): one warp per (request,
-// kv head), same vectorised merge as the fused path.
 template <int DH, int G>
-__global__ void attn_decode_combine(AttnParams p, int n_dec) {
-  const int lane = threadIdx.x % 32;
-  const int wid = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (wid >= n_dec * p.n_kv_heads) return;
-  const int d = wid / p.n_kv_heads, kvh = wid % p.n_kv_heads;
-  const int chunks = p.dec_chunks[d];
-  if (chunks <= 1) return;
-  const int base = p.dec_item_base[d] + kvh * chunks;
-  const int q_row = p.seq_q_start[p.dec_seq[d]];
-  __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
-  float wj[G], mj[G], lj[G], inv_l[G];
-#pragma unroll
-  for (int r = 0; r < G; ++r) {
-    const float2 ml = lane < chunks ? __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(base + lane) * G + r) * 2))
-                                    : make_float2(-INFINITY, 0.f);
-    mj[r] = ml.x;
-    lj[r] = ml.y;
-  }
-#pragma unroll
-  for (int r = 0; r < G; ++r) {
-    const float mm = warp_max(mj[r]);
-    wj[r] = (mj[r] == -INFINITY || mm == -INFINITY) ? 0.f : exp2f(mj[r] - mm);
-    const float ll = warp_sum(wj[r] * lj[r]);
-    inv_l[r] = ll > 0.f ? 1.f / ll : 0.f;
-  }
+TC_DEVICE void store_out_row(__nv_bfloat16* out_row, const float (&acc)[G][DH / 32], const float (&ll)[G]) {
   constexpr int V = DH / 32;
-  float acc[G][V] = {};
-  for (int j = 0; j < chunks; ++j) {
+  const int lane = threadIdx.x % 32;
 #pragma unroll
-    for (int r = 0; r < G; ++r) {
-      const float f = __shfl_sync(0xffffffffu, wj[r], j);
-      const float* src = p.ws_o + ((long long)(base + j) * G + r) * DH + lane * V;
-#pragma unroll
-      for (int e = 0; e < V; ++e) acc[r][e] += f * __ldcg(src + e);
+  for (int r = 0; r < G; ++r) {
+    const float inv = ll[r] > 0.f ? 1.f / ll[r] : 0.f;
+    __nv_bfloat16* dst = out_row + r * DH + lane * V;
+    if constexpr (V == 4) {
+      uint2 w;
+      w.x = pack_bf16(acc[r][0] * inv, acc[r][1] * inv);
+      w.y = pack_bf16(acc[r][2] * inv, acc[r][3] * inv);
+      *reinterpret_cast<uint2*>(dst) = w;
+    } else {
+      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc[r][0] * inv, acc[r][1] * inv);
     }
   }
+}
+
+template <int DH, int G>
+__global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  using SM = DecodeSmem<DH, G>;
+  constexpr int S = SM::kStages;
+  constexpr int V = DH / 32;
+  extern __shared__ uint8_t attn_smem_raw[];
+  __shared__ uint64_t full[S], empty[S], qfull[2], qempty[2];
+  const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
+  uint8_t* gbase = attn_smem_raw + (sbase - smem_u32(attn_smem_raw));
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int e_begin = p.dec_cta_off[blockIdx.x], e_end = p.dec_cta_off[blockIdx.x + 1];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&qfull[b], 1);
+      mbar_init(&qempty[b], kDecConsumers);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int qkv_ld = (p.n_heads + 2 * p.n_kv_heads) * DH;
+
+  if (warp == kDecConsumers) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) tma_prefetch_desc(&kv_map);
+    int g = 0;  // stages issued
+    for (int e0 = e_begin; e0 < e_end; e0 += 32) {
+      // lane j holds entry e0 + j and its segment descriptor
+      int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0);
+      if (e0 + lane < e_end) {
+        ent = p.dec_entries[e0 + lane];
+        sa = p.dec_seg_a[ent.x];
+      }
+      const int ne = min(32, e_end - e0);
+      for (int k = 0; k < ne; ++k) {
+        const int e = e0 + k - e_begin;  // local entry index
+        const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
+        const int bt_off = __shfl_sync(0xffffffffu, sa.x, k), q_row = __shfl_sync(0xffffffffu, sa.z, k);
+        const int kvh = __shfl_sync(0xffffffffu, sa.w, k);
+        if (lane == 0) {
+          const int b = e & 1;
+          mbar_wait(&qempty[b], ((e >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qfull[b], SM::kQBytes);
+          bulk_load(sbase + SM::kOffQ + b * ((SM::kQBytes + 127) / 128 * 128),
+                    p.qkv + (long long)q_row * qkv_ld + kvh * G * DH, SM::kQBytes, &qfull[b]);
+        }
+        for (int c = pg0; c < pg1; c += 32) {
+          // lane j: pool row of page c + j (coordinates computed 32 at a time, off the issue path)
+          const int row = c + lane < pg1 ? kv_row(p, p.block_tables[bt_off + c + lane], kvh) : 0;
+          const int n = min(32, pg1 - c);
+          for (int j = 0; j < n; ++j, ++g) {
+            const int rj = __shfl_sync(0xffffffffu, row, j);
+            if (lane == 0) {
+              const int st = g % S;
+              mbar_wait(&empty[st], ((g / S) & 1) ^ 1);
+              mbar_arrive_expect_tx(&full[st], SM::kStageBytes);
+              tma_load_3d(sbase + st * SM::kStageBytes, &kv_map, &full[st], KV_COORD(rj));
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int r_lo = lane / 4;
+  const bool ok_lo = r_lo < G;
+  const int c0 = (lane % 4) * 2;
+  float* part_o = reinterpret_cast<float*>(gbase + SM::kOffPart);
+  float* part_ml = reinterpret_cast<float*>(gbase + SM::kOffMl);
+  int g_base = 0;  // stages before the current entry
+  for (int e0 = e_begin; e0 < e_end; e0 += 32) {
+    int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0), sb = make_int4(0, 0, 0, 0);
+    if (e0 + lane < e_end) {
+      ent = p.dec_entries[e0 + lane];
+      sa = p.dec_seg_a[ent.x];
+      sb = p.dec_seg_b[ent.x];
+    }
+    const int ne = min(32, e_end - e0);
+    for (int k = 0; k < ne; ++k) {
+      const int e = e0 + k - e_begin;
+      const int seg = __shfl_sync(0xffffffffu, ent.x, k);
+      const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
+      const int part = __shfl_sync(0xffffffffu, ent.w, k);
+      const int kv_len = __shfl_sync(0xffffffffu, sa.y, k), q_row = __shfl_sync(0xffffffffu, sa.z, k);
+      const int kvh = __shfl_sync(0xffffffffu, sa.w, k);
+      const int n_parts = __shfl_sync(0xffffffffu, sb.x, k), ws_base = __shfl_sync(0xffffffffu, sb.y, k);
+      const int b = e & 1;
+      // q fragment (rows >= G are zero) from the entry's q slot
+      uint32_t qf[DH / 16][4];
+      mbar_wait(&qfull[b], (e >> 1) & 1);
+      {
+        const __nv_bfloat16* qs = reinterpret_cast<const __nv_bfloat16*>(gbase + SM::kOffQ +
+                                                                         b * ((SM::kQBytes + 127) / 128 * 128)) +
+                                  (ok_lo ? r_lo : 0) * DH + c0;
 #pragma unroll
-  for (int r = 0; r < G; ++r)
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          qf[ks][0] = ok_lo ? *reinterpret_cast<const uint32_t*>(qs + ks * 16) : 0u;
+          qf[ks][2] = ok_lo ? *reinterpret_cast<const uint32_t*>(qs + ks * 16 + 8) : 0u;
+          qf[ks][1] = qf[ks][3] = 0u;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[b]);
+      float o[DH / 8][4];
 #pragma unroll
-    for (int e = 0; e < V; ++e) out_row[r * DH + lane * V + e] = __float2bfloat16(acc[r][e] * inv_l[r]);
+      for (int c = 0; c < DH / 8; ++c) o[c][0] = o[c][1] = o[c][2] = o[c][3] = 0.f;
+      float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+      const int n = pg1 - pg0;
+      // this warp's stages of the entry: g_base + i with (g_base + i) % 4 == warp
+      for (int i = (warp - g_base % kDecConsumers + kDecConsumers) % kDecConsumers; i < n; i += kDecConsumers) {
+        const int g = g_base + i;
+        const int st = g % S;
+        mbar_wait(&full[st], (g / S) & 1);
+        const uint32_t k_smem = sbase + st * SM::kStageBytes;
+        float s[2][4];
+        attn_qk<DH, 2>(qf, k_smem, 0, s);
+        attn_softmax_step<DH, 2>(s, (pg0 + i) * kPage, kv_len, kv_len, p.scale_log2, m, l, o);
+        attn_pv<DH, 2>(s, k_smem, 0, o);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      g_base += n;
+      l[0] += __shfl_xor_sync(0xffffffffu, l[0], 1);
+      l[0] += __shfl_xor_sync(0xffffffffu, l[0], 2);
+      // publish this warp's partial state
+      float* po = part_o + ((b * kDecConsumers + warp) * G) * DH;
+      float* pml = part_ml + ((b * kDecConsumers + warp) * G) * 2;
+      if (ok_lo) {
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(po + r_lo * DH + c * 8 + c0) = make_float2(o[c][0], o[c][1]);
+        if (lane % 4 == 0) *reinterpret_cast<float2*>(pml + r_lo * 2) = make_float2(m[0], l[0]);
+      }
+      consumer_bar();
+      if (warp != e % kDecConsumers) continue;
+      // merging warp: combine the 4 warps' states of this entry
+      const float* bo = part_o + (b * kDecConsumers * G) * DH;
+      const float* bml = part_ml + (b * kDecConsumers * G) * 2;
+      float acc[G][V], mm[G], ll[G];
+      merge_partials<DH, G>(
+          kDecConsumers, [&](int j, int r) { return *reinterpret_cast<const float2*>(bml + (j * G + r) * 2); },
+          [&](int j, int r, float* d) {
+            const float* src = bo + (j * G + r) * DH + lane * V;
+#pragma unroll
+            for (int x = 0; x < V; ++x) d[x] = src[x];
+          },
+          acc, mm, ll);
+      __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
+      if (n_parts == 1) {
+        store_out_row<DH, G>(out_row, acc, ll);
+        continue;
+      }
+      // segment cut by a CTA boundary: publish the CTA's part; the last arriver combines
+      const int slot = ws_base + part;
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        float* dst = p.ws_o + ((long long)slot * G + r) * DH + lane * V;
+#pragma unroll
+        for (int x = 0; x < V; ++x) dst[x] = acc[r][x];
+        if (lane == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)slot * G + r) * 2) = make_float2(mm[r], ll[r]);
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();
+        int* cnt = p.dec_cnt + seg;
+        last = atomicAdd(cnt, 1) == n_parts - 1;
+        if (last) *cnt = 0;  // ready for the next layer / step
+      }
+      if (!__shfl_sync(0xffffffffu, last, 0)) continue;
+      __threadfence();
+      merge_partials<DH, G>(
+          n_parts,
+          [&](int j, int r) { return __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(ws_base + j) * G + r) * 2)); },
+          [&](int j, int r, float* d) {
+            const float* src = p.ws_o + ((long long)(ws_base + j) * G + r) * DH + lane * V;
+            if constexpr (V == 4) {
+              const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+              d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+            } else {
+              const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+              d[0] = t.x; d[1] = t.y;
+            }
+          },
+          acc, mm, ll);
+      store_out_row<DH, G>(out_row, acc, ll);
+    }
+  }
 }
 
 }  // namespace tc

@@ -204,7 +204,7 @@ __device__ __forceinline__ void epi_qkv_rope_row(const GemmArgs& args, int m_in,
     } else {
       const int kvh = head - r.n_heads - (is_k ? 0 : r.n_kv_heads);
       dst = r.kv + (size_t)page * r.page_stride +
-            ((((size_t)r.layer * 2 + (is_k ? 0 : 1)) * r.n_kv_heads + kvh) * r.page_size + slot) * DH;
+            ((((size_t)r.layer * r.n_kv_heads + kvh) * 2 + (is_k ? 0 : 1)) * r.page_size + slot) * DH;
     }
 #pragma unroll 1
     for (int c = 0; c < hc; ++c) {
@@ -562,7 +562,7 @@ __global__ void finish_qkv_rope(const float* __restrict__ scr, int M, QkvRopeArg
       const int page = r.block_tables[r.seq_bt_off[seq] + pos / r.page_size];
       const int kvh = head - r.n_heads - (is_k ? 0 : r.n_kv_heads);
       dst = r.kv + (size_t)page * r.page_stride +
-            ((((size_t)r.layer * 2 + (is_k ? 0 : 1)) * r.n_kv_heads + kvh) * r.page_size + pos % r.page_size) * r.head_dim;
+            ((((size_t)r.layer * r.n_kv_heads + kvh) * 2 + (is_k ? 0 : 1)) * r.page_size + pos % r.page_size) * r.head_dim;
     }
     dst[j] = __float2bfloat16(lo);
     dst[j + half] = __float2bfloat16(hi);

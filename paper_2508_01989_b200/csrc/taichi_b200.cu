@@ -144,9 +144,9 @@ void init_kernel_attrs(int dev) {
   attr((const void*)tc::attn_prefill<64, 2>, tc::PrefillSmem<64>::kBytes);
   attr((const void*)tc::attn_prefill<128, 4>, tc::PrefillSmem<128>::kBytes);
   attr((const void*)tc::attn_prefill<128, 5>, tc::PrefillSmem<128>::kBytes);
-  attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128>::kBytes);
-  attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128>::kBytes);
+  attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64, 2>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128, 4>::kBytes);
+  attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128, 5>::kBytes);
   done.insert(dev);
 }
 
@@ -402,7 +402,7 @@ struct tc_instance {
   __nv_bfloat16* kv = nullptr;
   int64_t page_elems = 0, n_pages = 0;
   std::vector<int32_t> free_pages;
-  CUtensorMap kv_map;  // 3-D view {64 dims, head_dim/64, pool rows} for TMA page loads
+  CUtensorMap kv_map;  // 3-D view {64 dims, pool rows, head_dim/64 halves}; box = one (K, V) page pair
   std::unordered_map<int64_t, std::vector<int32_t>> tables;
   // activations
   int qkv_n = 0;
@@ -586,7 +586,7 @@ void alloc_buffers(tc_instance* I) {
   // metadata: 3T + 4S + qblocks(<= T + S) * 2 + S (dec) + S (logit rows) + block tables
   const int64_t max_pages_per_seq = (I->desc.max_context + I->desc.page_size - 1) / I->desc.page_size;
   I->meta_ints = 3 * (size_t)T + 4 * (size_t)S + 2 * (size_t)(T + S) + 4 * (size_t)S +
-                 4 * (size_t)kMaxDecodeItems + (size_t)S * max_pages_per_seq + 128;
+                 12 * (size_t)S * m.n_kv_heads + 4 * 1024 + 1024 + (size_t)S * max_pages_per_seq + 128;
   TC_CUDA(cudaMallocHost(&I->meta_host, I->meta_ints * 4));
   TC_CUDA(cudaMalloc(&I->meta_dev, I->meta_ints * 4));
   TC_CUDA(cudaEventCreate(&I->ev_start));
@@ -639,33 +639,24 @@ struct ProfScope {
 };
 
 template <int DH, int G>
-void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid, bool combine) {
+void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int hk = I->d.n_kv_heads;
   if (n_qblk > 0) {
     tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kPrefillThreads, tc::PrefillSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
     ++I->launches;
   }
   if (n_dec > 0) {
-    tc::attn_decode<DH, G><<<dec_grid, tc::kDecodeWarps * 32, tc::DecodeSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
+    tc::attn_decode<DH, G><<<dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream>>>(I->kv_map, p);
     ++I->launches;
-#if TC_DECODE_FUSED_MERGE
-    (void)combine;  // split requests are merged inside attn_decode (last arriver)
-#else
-    if (combine) {
-      const int warps = n_dec * hk;
-      tc::attn_decode_combine<DH, G><<<(warps + 3) / 4, 128, 0, I->stream>>>(p, n_dec);
-      ++I->launches;
-    }
-#endif
   }
   TC_CUDA(cudaGetLastError());
 }
 
-void dispatch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid, bool combine) {
+void dispatch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int G = I->d.n_heads / I->d.n_kv_heads;
-  if (I->d.head_dim == 64 && G == 2) launch_attention<64, 2>(I, p, n_qblk, n_dec, dec_grid, combine);
-  else if (I->d.head_dim == 128 && G == 4) launch_attention<128, 4>(I, p, n_qblk, n_dec, dec_grid, combine);
-  else if (I->d.head_dim == 128 && G == 5) launch_attention<128, 5>(I, p, n_qblk, n_dec, dec_grid, combine);
+  if (I->d.head_dim == 64 && G == 2) launch_attention<64, 2>(I, p, n_qblk, n_dec, dec_grid);
+  else if (I->d.head_dim == 128 && G == 4) launch_attention<128, 4>(I, p, n_qblk, n_dec, dec_grid);
+  else if (I->d.head_dim == 128 && G == 5) launch_attention<128, 5>(I, p, n_qblk, n_dec, dec_grid);
   else throw TcFail{TC_ERR_INVALID, "unsupported attention shape"};
 }
 
@@ -701,22 +692,14 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   }
   n_logit += n_dec;
   for (int i = 0; i < n_dec; ++i) n_bt += st->decode[i].pos / ps + 1;
-  // decode split-KV work items: (request, kv head, run of <= ppi pages). ppi balances ~4 items
-  // per resident warp (2 CTAs x 4 warps per SM) and caps the item count.
-  long long page_heads = 0;
-  for (int i = 0; i < n_dec; ++i) page_heads += (long long)(st->decode[i].pos / ps + 1) * m.n_kv_heads;
-  const long long dec_warps = 2LL * I->sms * tc::kDecodeWarps;
-  int ppi = (int)std::max<long long>(4, (page_heads + 4 * dec_warps - 1) / (4 * dec_warps));
-  auto count_items = [&](int per) {
-    long long n = 0;
-    for (int i = 0; i < n_dec; ++i) n += (long long)m.n_kv_heads * ((st->decode[i].pos / ps + 1 + per - 1) / per);
-    return n;
-  };
-  int max_pages = 1;
-  for (int i = 0; i < n_dec; ++i) max_pages = std::max(max_pages, st->decode[i].pos / ps + 1);
-  ppi = std::max(ppi, (max_pages + 31) / 32);  // <= 32 items per (request, kv head): one merge round trip
-  while (count_items(ppi) > kMaxDecodeItems) ppi *= 2;
-  const int n_items = (int)count_items(ppi);
+  // decode work (attn_decode): segments (decode j, kv head h) = seg j * Hk + h, laid end to end
+  // as one stream of page-heads; CTA c takes pages [W*c/NC, W*(c+1)/NC).
+  const int n_seg = n_dec * m.n_kv_heads;
+  long long W = 0;
+  for (int i = 0; i < n_dec; ++i) W += (long long)(st->decode[i].pos / ps + 1) * m.n_kv_heads;
+  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(I->sms, (W + 7) / 8)) : 0;
+  // entries: one per (CTA, segment overlap); at most n_seg + dec_grid
+  const int max_entries = n_seg + dec_grid;
   // layout of the metadata block
   int32_t* h = I->meta_host;
   size_t off = 0;
@@ -726,9 +709,9 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     return o;
   };
   const size_t o_tok = take(T), o_pos = take(T), o_rseq = take(T), o_qs = take(n_seq), o_ql = take(n_seq),
-               o_p0 = take(n_seq), o_bo = take(n_seq), o_qbs = take(n_qblk), o_qbo = take(n_qblk), o_dseq = take(n_dec),
-               o_lrow = take(n_logit), o_bt = take(n_bt), o_items = take(4 * (size_t)n_items), o_ibase = take(n_dec),
-               o_ichunks = take(n_dec);
+               o_p0 = take(n_seq), o_bo = take(n_seq), o_qbs = take(n_qblk), o_qbo = take(n_qblk),
+               o_lrow = take(n_logit), o_bt = take(n_bt), o_sega = take(4 * (size_t)n_seg), o_segb = take(4 * (size_t)n_seg),
+               o_ent = take(4 * (size_t)max_entries), o_ctaoff = take((size_t)dec_grid + 1);
   TC_REQUIRE(off <= I->meta_ints, "step: metadata overflow");
   int row = 0, qb = 0, lr = 0, bt = 0;
   for (int i = 0; i < n_pf; ++i) {
@@ -769,28 +752,57 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     h[o_tok + row] = di.token_id;
     h[o_pos + row] = di.pos;
     h[o_rseq + row] = s;
-    h[o_dseq + j] = s;
     h[o_lrow + lr++] = row;
     ++row;
   }
-  bool any_split = false;
-  {
-    int it = 0;
-    for (int j = 0; j < n_dec; ++j) {
-      const int pages = st->decode[j].pos / ps + 1;
-      const int chunks = (pages + ppi - 1) / ppi;
-      h[o_ibase + j] = it;
-      h[o_ichunks + j] = chunks;
-      any_split = any_split || chunks > 1;
-      for (int kh = 0; kh < m.n_kv_heads; ++kh)
-        for (int c = 0; c < chunks; ++c) {
-          int32_t* e = h + o_items + 4 * (size_t)it++;
-          e[0] = h[o_bo + n_pf + j];  // block-table offset of the request
-          e[1] = kh | (j << 8);
-          e[2] = c * ppi;
-          e[3] = std::min(pages, (c + 1) * ppi);
+  if (n_dec) {
+    // segment descriptors
+    int32_t* sa = h + o_sega;
+    int32_t* sb = h + o_segb;
+    for (int j = 0; j < n_dec; ++j)
+      for (int kh = 0; kh < m.n_kv_heads; ++kh) {
+        const int sg = j * m.n_kv_heads + kh;
+        sa[4 * sg + 0] = h[o_bo + n_pf + j];
+        sa[4 * sg + 1] = st->decode[j].pos + 1;
+        sa[4 * sg + 2] = h[o_qs + n_pf + j];
+        sa[4 * sg + 3] = kh;
+        sb[4 * sg + 0] = 0;
+        sb[4 * sg + 1] = 0;
+        sb[4 * sg + 2] = sb[4 * sg + 3] = 0;
+      }
+    // walk the page stream, cutting it at CTA boundaries
+    int32_t* ent = h + o_ent;
+    int ne = 0, sg = 0, pg = 0;  // cursor: segment, page within it
+    auto seg_pages = [&](int g) { return st->decode[g / m.n_kv_heads].pos / ps + 1; };
+    for (int c = 0; c < dec_grid; ++c) {
+      h[o_ctaoff + c] = ne;
+      long long left = W * (c + 1) / dec_grid - W * c / dec_grid;
+      while (left > 0) {
+        const int np = seg_pages(sg);
+        const int take_n = (int)std::min<long long>(left, np - pg);
+        ent[4 * ne + 0] = sg;
+        ent[4 * ne + 1] = pg;
+        ent[4 * ne + 2] = pg + take_n;
+        ent[4 * ne + 3] = sb[4 * sg + 0]++;  // part index; the count becomes the segment's parts
+        ++ne;
+        pg += take_n;
+        left -= take_n;
+        if (pg == np) {
+          ++sg;
+          pg = 0;
         }
+      }
     }
+    h[o_ctaoff + dec_grid] = ne;
+    TC_REQUIRE(ne <= max_entries, "step: decode entry overflow");
+    int slots = 0;
+    for (int g = 0; g < n_seg; ++g) {
+      if (sb[4 * g + 0] > 1) {
+        sb[4 * g + 1] = slots;
+        slots += sb[4 * g + 0];
+      }
+    }
+    TC_REQUIRE(slots <= kMaxDecodeItems, "step: decode partial slots overflow");
   }
   cudaStream_t s = I->stream;
   DeviceGuard dg(I->desc.device);
@@ -801,7 +813,6 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   TC_CUDA(cudaMemcpyAsync(I->meta_dev, h, off * 4, cudaMemcpyHostToDevice, s));
   const int32_t* dm = I->meta_dev;
 
-  const int dec_grid = (int)std::max<long long>(1, std::min<long long>(2LL * I->sms, (n_items + tc::kDecodeWarps - 1) / tc::kDecodeWarps));
 
   {
     ProfScope ps_(I, "embed");
@@ -823,11 +834,10 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   ap.block_tables = dm + o_bt;
   ap.qblk_seq = dm + o_qbs;
   ap.qblk_off = dm + o_qbo;
-  ap.dec_seq = dm + o_dseq;
-  ap.dec_items = reinterpret_cast<const int4*>(dm + o_items);
-  ap.n_items = n_items;
-  ap.dec_item_base = dm + o_ibase;
-  ap.dec_chunks = dm + o_ichunks;
+  ap.dec_seg_a = reinterpret_cast<const int4*>(dm + o_sega);
+  ap.dec_seg_b = reinterpret_cast<const int4*>(dm + o_segb);
+  ap.dec_entries = reinterpret_cast<const int4*>(dm + o_ent);
+  ap.dec_cta_off = dm + o_ctaoff;
   ap.ws_o = I->attn_ws_o;
   ap.dec_cnt = I->attn_cnt;
   ap.ws_ml = I->attn_ws_ml;
@@ -874,7 +884,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     {
       ProfScope p_(I, "attn");
       ap.layer = l;
-      dispatch_attention(I, ap, n_qblk, n_dec, dec_grid, any_split);
+      dispatch_attention(I, ap, n_qblk, n_dec, dec_grid);
     }
     {
       ProfScope p_(I, "gemm_o");
@@ -1083,17 +1093,12 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     {
       const uint64_t rows = (uint64_t)I->n_pages * m.n_layers * 2 * m.n_kv_heads * desc->page_size;
       TC_REQUIRE(rows < (1ull << 31), "create: KV pool too large for 32-bit TMA row coordinates");
-      // dims {64 dims, pool rows, head_dim/64 halves}: each half of a 16-row block lands as a
-      // separate 16-line 128 B-swizzled slab (bank-conflict-free ldmatrix, K-major SW128 layout)
-#if TC_KV_SLAB
+      // dims {64 dims, pool rows, head_dim/64 halves}: one box = the adjacent K and V blocks of a
+      // (page, layer, kv head); each 64-dim half lands as a separate 32-line 128 B-swizzled slab
+      // (bank-conflict-free ldmatrix, K-major SW128 layout)
       const cuuint64_t dims[3] = {64, rows, (cuuint64_t)(m.head_dim / 64)};
       const cuuint64_t strides[2] = {(cuuint64_t)m.head_dim * 2, 128};
-      const cuuint32_t box[3] = {64, (cuuint32_t)desc->page_size, (cuuint32_t)(m.head_dim / 64)};
-#else
-      const cuuint64_t dims[3] = {64, (cuuint64_t)(m.head_dim / 64), rows};
-      const cuuint64_t strides[2] = {128, (cuuint64_t)m.head_dim * 2};
-      const cuuint32_t box[3] = {64, (cuuint32_t)(m.head_dim / 64), (cuuint32_t)desc->page_size};
-#endif
+      const cuuint32_t box[3] = {64, (cuuint32_t)(2 * desc->page_size), (cuuint32_t)(m.head_dim / 64)};
       const cuuint32_t estr[3] = {1, 1, 1};
       const CUresult r = tensor_map_encoder()(&I->kv_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, I->kv, dims, strides, box,
                                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -136,6 +136,31 @@ def test_tiny_mixed_batches(tiny):
         inst.kv_release(rid)
 
 
+@pytest.mark.parametrize("lengths", [(3500,), (1, 15, 16, 17, 33, 700, 3500), tuple(range(1, 60, 3))])
+def test_tiny_decode_page_stream_splits(tiny, lengths):
+    """Decode attention work split (attn_decode): contexts of 1..3500 tokens in one step; a lone
+    3500-token request is cut across > 32 CTAs (multi-part global merge), short ones share CTAs."""
+    inst, model = tiny
+    reqs = {}
+    for k, n in enumerate(lengths):
+        rid = 200 + k
+        prompt = mr.prompt_tokens(11, rid, n, 1024)
+        for s0 in range(0, n, 2048):
+            out = inst.step(prefill=[(rid, s0, prompt[s0:s0 + 2048], s0 + 2048 >= n)])
+        reqs[rid] = [Follower(model, prompt), int(out.sampled[0]), n]
+        reqs[rid][0].check(reqs[rid][1])
+    for _ in range(2):
+        dec = [(rid, r[2], r[1]) for rid, r in reqs.items()]
+        o = inst.step(decode=dec, keep_logits=True)
+        for k, (rid, pos, tok) in enumerate(dec):
+            f = reqs[rid][0]
+            f.feed([tok])
+            f.check(int(o.sampled[k]), o.logits[k])
+            reqs[rid][1], reqs[rid][2] = int(o.sampled[k]), pos + 1
+    for rid in reqs:
+        inst.kv_release(rid)
+
+
 def test_kv_pages_released_and_reused(tiny):
     inst, _ = tiny
     _, free0 = inst.kv_stats()
