@@ -320,6 +320,275 @@ __global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_
   }
 }
 
+// ============================================================== chunked prefill (tcgen05)
+// CTA = one q tile of 128 rows x one kv head: rows r = (token r / G, head r % G) of TT = 128/G
+// consecutive tokens of a prefill slice (the GQA group shares every K/V byte the CTA loads).
+// Per 128-key tile j (8 pages):
+//   MMA warp   S_j = Q K_j^T            (M=128, N=128, K=DH; Q, K in smem, SW128 K-major) -> TMEM S[j&1]
+//   softmax    8 warps, 2 threads per row (TMEM lane): warp w < 4 takes keys 0-63 of rows
+//              32w.., warp w + 4 keys 64-127; the pair exchanges its row max through smem, then
+//              writes bf16 P_j over its own S_j columns in TMEM (two keys per 32-bit column)
+//   MMA warp   O_j = P_j V_j            (A = P from TMEM, B = V MN-major SW128) -> TMEM O[j&1]
+//   softmax    o = o * 2^(m_prev - m_j) + O_j in registers, each thread of a row pair half of the
+//              head dims (one tile behind, off the MMA's path)
+// The MMA warp issues S_{j+1} before waiting for P_j, so QK^T of the next tile overlaps the
+// softmax of the current one. K and V tiles stream through separate TMA rings (3 / 2 stages, one
+// 2 KiB box per page and 64-dim half), K_j is released when S_j completes, V_j when O_j does.
+constexpr int kPfKeys = 128;
+constexpr int kPfThreads = 352;  // warps 0-7 softmax/epilogue (2 threads per row), 8 K producer, 9 V producer,
+                                 // 10 MMA issuer + TMEM owner
+constexpr int kPfStages = 3;   // K ring depth
+constexpr int kPfVStages = 2;  // V ring depth (V_j is consumed one MMA later than K_j)
+
+template <int DH, int G>
+struct PfCfg {
+  static constexpr int TT = 128 / G;                 // tokens per q tile
+  static constexpr int kHalves = DH / 64;
+  static constexpr int kSlab = 128 * 128;            // 128 rows x 128 B
+  static constexpr int kQBytes = kHalves * kSlab;    // Q [128 rows][DH]
+  static constexpr int kKBytes = kHalves * kSlab;    // K [128 keys][DH] (one slab per 64-dim half)
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kQBytes;
+  static constexpr int kOffV = kOffK + kPfStages * kKBytes;
+  static constexpr int kOffX = kOffV + kPfVStages * kKBytes;  // row-max / row-sum exchange [2][2][128] f32
+  static constexpr int kBytes = kOffX + 2 * 2 * 128 * 4 + 1024;
+  static constexpr uint32_t kQTx = kHalves * TT * G * 128;  // bytes the Q boxes deliver
+  static_assert(kBytes <= 227 * 1024, "prefill smem");
+};
+
+template <int DH, int G>
+__global__ void __launch_bounds__(kPfThreads, 1)
+    attn_prefill_tc(const __grid_constant__ CUtensorMap kv2_map, const __grid_constant__ CUtensorMap q_map, AttnParams p) {
+  using C = PfCfg<DH, G>;
+  constexpr int TT = C::TT;
+  extern __shared__ uint8_t attn_smem_raw[];
+  __shared__ uint64_t q_full, k_full[kPfStages], k_empty[kPfStages], v_full[kPfVStages], v_empty[kPfVStages];
+  __shared__ uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int seq = p.qblk_seq[blockIdx.x];
+  const int qoff = p.qblk_off[blockIdx.x];
+  const int kvh = blockIdx.y;
+  const int q_start = p.seq_q_start[seq], q_len = p.seq_q_len[seq], pos0 = p.seq_pos0[seq];
+  const int* bt = p.block_tables + p.seq_bt_off[seq];
+  const int kv_end = pos0 + min(qoff + TT, q_len);
+  const int n_tiles = (kv_end + kPfKeys - 1) / kPfKeys;
+  const int n_pages = (kv_end + kPage - 1) / kPage;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&q_full, 1);
+    for (int s = 0; s < kPfStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kPfVStages; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 256);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 10) tmem_alloc(&tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;  // S0 @0, S1 @128, O0 @256, O1 @384
+
+  if (warp == 8 || warp == 9) {
+    // ------------------------------------------------------------ TMA producers: warp 8 streams
+    // Q then the K tiles, warp 9 the V tiles, so a K load never waits for a V slot (V_j frees one
+    // MMA later than K_j)
+    const bool is_v = warp == 9;
+    if (lane == 0 && !is_v) {
+      tma_prefetch_desc(&kv2_map);
+      tma_prefetch_desc(&q_map);
+      mbar_arrive_expect_tx(&q_full, C::kQTx);
+#pragma unroll
+      for (int h = 0; h < C::kHalves; ++h)
+        tma_load_3d(sbase + C::kOffQ + h * C::kSlab, &q_map, &q_full, h * 64, kvh * G, q_start + qoff);
+    }
+    auto page_id = [&](int gp) { return bt[gp < n_pages ? gp : 0]; };  // beyond the sequence: masked
+    int cur = lane < 8 ? page_id(lane) : 0;
+    const int depth = is_v ? kPfVStages : kPfStages;
+    uint64_t* fullb = is_v ? v_full : k_full;
+    uint64_t* emptyb = is_v ? v_empty : k_empty;
+    const uint32_t ring = sbase + (is_v ? C::kOffV : C::kOffK);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int row = kv_row(p, cur, kvh) + (is_v ? kPage : 0);  // lanes 0-7: page 8j + lane
+      if (lane < 8 && j + 1 < n_tiles) cur = page_id((j + 1) * 8 + lane);
+      int rows[8];
+#pragma unroll
+      for (int pg = 0; pg < 8; ++pg) rows[pg] = __shfl_sync(0xffffffffu, row, pg);
+      if (lane == 0) {
+        const int st = j % depth;
+        mbar_wait(&emptyb[st], ((j / depth) & 1) ^ 1);
+        mbar_arrive_expect_tx(&fullb[st], C::kKBytes);
+        const uint32_t d = ring + st * C::kKBytes;
+#pragma unroll
+        for (int pg = 0; pg < 8; ++pg)
+#pragma unroll
+          for (int h = 0; h < C::kHalves; ++h)
+            tma_load_2d_u32(d + h * C::kSlab + pg * 2048, &kv2_map, &fullb[st], h * 64, rows[pg]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, kPfKeys);
+    constexpr uint32_t idesc_o = umma_idesc_bf16_bmn(128, DH);
+    auto issue_pv = [&](int i) {
+      const int st = i % kPfVStages;
+      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+      mbar_wait(&v_full[st], (i / kPfVStages) & 1);
+      if (i >= 2) mbar_wait(&o_empty[i & 1], ((i - 2) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t vb = sbase + C::kOffV + st * C::kKBytes;
+        // P of keys 0-63 sits at S columns 0-31, keys 64-127 at S columns 64-95 (each softmax
+        // thread overwrites only the S columns it has read itself)
+#pragma unroll
+        for (int kk = 0; kk < kPfKeys / 16; ++kk)
+          umma_bf16_tmem_a(tmem + 256 + (i & 1) * 128, tmem + (i & 1) * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
+                           umma_smem_desc_mn128(vb + kk * 2048, C::kSlab, 1024), idesc_o, kk > 0 ? 1u : 0u);
+        umma_commit(&o_full[i & 1]);
+        umma_commit(&v_empty[st]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(&q_full, 0);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j % kPfStages;
+      mbar_wait(&k_full[st], (j / kPfStages) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t kb = sbase + C::kOffK + st * C::kKBytes;
+#pragma unroll
+        for (int h = 0; h < C::kHalves; ++h)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + (j & 1) * 128, umma_smem_desc<128>(sbase + C::kOffQ + h * C::kSlab + k * 32),
+                      umma_smem_desc<128>(kb + h * C::kSlab + k * 32), idesc_s, (h | k) ? 1u : 0u);
+        umma_commit(&s_full[j & 1]);
+        umma_commit(&k_empty[st]);
+      }
+      __syncwarp();
+      if (j >= 1) issue_pv(j - 1);
+    }
+    issue_pv(n_tiles - 1);
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    constexpr int HD = DH / 2;             // head dims per thread
+    const int quarter = warp & 3, half = warp >> 2;
+    const int r = quarter * 32 + lane;     // row == TMEM lane
+    const int t = r / G, g = r % G;
+    const bool valid = r < TT * G && qoff + t < q_len;
+    const int lim = valid ? pos0 + qoff + t + 1 : 0;  // causal: keys < lim
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float* xmax = reinterpret_cast<float*>(attn_smem_raw + (sbase - smem_u32(attn_smem_raw)) + C::kOffX);  // [2][2][128]
+    float o[HD];
+#pragma unroll
+    for (int c = 0; c < HD; ++c) o[c] = 0.f;
+    float m = -INFINITY, l = 0.f, m_o = -INFINITY, m_tile0 = 0.f, m_tile1 = 0.f;  // base of P_j, j even / odd
+    // iteration j: softmax of tile j (if any), then fold O_{j-1} into o (one tile behind)
+    for (int j = 0; j <= n_tiles; ++j) {
+      if (j < n_tiles) {
+        mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t s_addr = tmem + lane_off + (j & 1) * 128 + half * 64;
+        const int key0 = j * kPfKeys + half * 64;
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(s_addr + c * 32, v);
+          tmem_ld_wait();
+          const int kc = key0 + c * 32;
+#pragma unroll
+          for (int x = 0; x < 32; ++x)
+            if (kc + x < lim) mx4[x & 3] = fmaxf(mx4[x & 3], __uint_as_float(v[x]));
+        }
+        // pair exchange of the row max (buffer j & 1; the partner reads it before the next barrier)
+        const float mine = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
+        xmax[((j & 1) * 2 + half) * 128 + r] = mine;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        const float mx = fmaxf(m, fmaxf(mine, xmax[((j & 1) * 2 + (half ^ 1)) * 128 + r]));
+        const float base = mx == -INFINITY ? 0.f : mx;
+        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(s_addr + c * 32, v);
+          tmem_ld_wait();
+          uint32_t pk[16];
+          const int kc = key0 + c * 32;
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            const float p0 = kc + 2 * x < lim ? fast_exp2(__uint_as_float(v[2 * x]) * p.scale_log2 - base) : 0.f;
+            const float p1 = kc + 2 * x + 1 < lim ? fast_exp2(__uint_as_float(v[2 * x + 1]) * p.scale_log2 - base) : 0.f;
+            sum4[x & 3] += p0 + p1;
+            pk[x] = pack_bf16(p0, p1);
+          }
+          tmem_st_32x32b_x16(s_addr + c * 16, pk);  // P over this thread's already-read S columns
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[j & 1]);
+        const float sum = (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+        l = (m == -INFINITY ? 0.f : l * fast_exp2(m - base)) + sum;
+        m = mx;
+        if (j & 1) m_tile1 = base; else m_tile0 = base;
+      }
+      if (j >= 1) {
+        const int i = j - 1;
+        mbar_wait(&o_full[i & 1], (i >> 1) & 1);
+        tc_fence_after();
+        const float mt = (i & 1) ? m_tile1 : m_tile0;
+        const float corr = m_o == -INFINITY ? 0.f : fast_exp2(m_o - mt);
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem + lane_off + 256 + (i & 1) * 128 + half * HD + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int x = 0; x < 32; ++x) o[c * 32 + x] = o[c * 32 + x] * corr + __uint_as_float(v[x]);
+        }
+        m_o = mt;
+        tc_fence_before();
+        mbar_arrive(&o_empty[i & 1]);
+      }
+    }
+    // row sum = both halves' partial sums (same base)
+    xmax[half * 128 + r] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    const float l_row = l + xmax[(half ^ 1) * 128 + r];
+    if (valid) {
+      const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
+      __nv_bfloat16* dst = p.out + (long long)(q_start + qoff + t) * p.n_heads * DH + (kvh * G + g) * DH + half * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 8; ++c) {
+        uint4 w;
+        w.x = pack_bf16(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
+        w.y = pack_bf16(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
+        w.z = pack_bf16(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
+        w.w = pack_bf16(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+        st_global_v4(dst + c * 8, w);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 10) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ============================================================== decode
 // Work decomposition (host, step_launch): a SEGMENT is (decode request, kv head) and covers
 // that request's KV pages 0..ceil(kv_len/16)-1. All segments' pages, laid end to end, form one

@@ -102,6 +102,16 @@ CUtensorMap make_kmajor_map(const void* base, uint64_t rows, uint64_t cols, uint
   return m;
 }
 
+CUtensorMap encode_map(void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+  CUtensorMap m;
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TcFail{TC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+  return m;
+}
+
 // ------------------------------------------------------------------ GEMM dispatch
 int device_sms(int dev) {
   static std::mutex mu;
@@ -144,6 +154,9 @@ void init_kernel_attrs(int dev) {
   attr((const void*)tc::attn_prefill<64, 2>, tc::PrefillSmem<64>::kBytes);
   attr((const void*)tc::attn_prefill<128, 4>, tc::PrefillSmem<128>::kBytes);
   attr((const void*)tc::attn_prefill<128, 5>, tc::PrefillSmem<128>::kBytes);
+  attr((const void*)tc::attn_prefill_tc<64, 2>, tc::PfCfg<64, 2>::kBytes);
+  attr((const void*)tc::attn_prefill_tc<128, 4>, tc::PfCfg<128, 4>::kBytes);
+  attr((const void*)tc::attn_prefill_tc<128, 5>, tc::PfCfg<128, 5>::kBytes);
   attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64, 2>::kBytes);
   attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128, 4>::kBytes);
   attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128, 5>::kBytes);
@@ -403,6 +416,8 @@ struct tc_instance {
   int64_t page_elems = 0, n_pages = 0;
   std::vector<int32_t> free_pages;
   CUtensorMap kv_map;  // 3-D view {64 dims, pool rows, head_dim/64 halves}; box = one (K, V) page pair
+  CUtensorMap kv2_map;  // 2-D view {head_dim, pool rows}; box = one 64-dim half of one K or V block
+  CUtensorMap q_map;    // 3-D view of the q heads of the qkv buffer {head_dim, q heads, rows}
   std::unordered_map<int64_t, std::vector<int32_t>> tables;
   // activations
   int qkv_n = 0;
@@ -560,6 +575,13 @@ void alloc_buffers(tc_instance* I) {
   I->map_attn = make_kmajor_map(I->attn_out, Tp, (uint64_t)m.n_heads * m.head_dim, 128);
   I->map_act = make_kmajor_map(I->act, Tp, m.ffn_dim, 128);
   I->map_lm_in = make_kmajor_map(I->lm_in, Sp, dm, 128);
+  {
+    const int G = m.n_heads / m.n_kv_heads;
+    const cuuint64_t dims[3] = {(cuuint64_t)m.head_dim, (cuuint64_t)m.n_heads, (cuuint64_t)Tp};
+    const cuuint64_t strides[2] = {(cuuint64_t)m.head_dim * 2, (cuuint64_t)I->qkv_n * 2};
+    const cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)(128 / G)};
+    I->q_map = encode_map(I->qkv, 3, dims, strides, box);
+  }
   TC_CUDA(cudaMalloc(&I->stream_scr, (size_t)kStreamRows * std::max<int64_t>(I->qkv_n, 2 * (int64_t)m.ffn_dim) * 4));
   // stream-K partial slots + tile counters (counters must start at zero)
   TC_CUDA(cudaMalloc(&I->sk.ws, kSkWsBytes));
@@ -642,7 +664,12 @@ template <int DH, int G>
 void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int hk = I->d.n_kv_heads;
   if (n_qblk > 0) {
+#if TC_PREFILL_MMA_SYNC
     tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kPrefillThreads, tc::PrefillSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
+#else
+    tc::attn_prefill_tc<DH, G><<<dim3(n_qblk, hk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream>>>(I->kv2_map,
+                                                                                                       I->q_map, p);
+#endif
     ++I->launches;
   }
   if (n_dec > 0) {
@@ -683,7 +710,11 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   for (int i = 0; i < n_dec; ++i) ensure_pages(I, st->decode[i].req_id, st->decode[i].pos + 1);
 
   const int G = m.n_heads / m.n_kv_heads;
+#if TC_PREFILL_MMA_SYNC
   const int tpc = 4 * (16 / G);  // prefill tokens per attention CTA
+#else
+  const int tpc = 128 / G;  // prefill tokens per attention CTA (one 128-row q tile)
+#endif
   int n_qblk = 0, n_logit = 0, n_bt = 0;
   for (int i = 0; i < n_pf; ++i) {
     n_qblk += (st->prefill[i].n_tokens + tpc - 1) / tpc;
@@ -1104,6 +1135,13 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
                                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw TcFail{TC_ERR_CUDA, "KV tensor map encode failed: " + std::to_string((int)r)};
+    }
+    {
+      const uint64_t rows = (uint64_t)I->n_pages * m.n_layers * 2 * m.n_kv_heads * desc->page_size;
+      const cuuint64_t dims[2] = {(cuuint64_t)m.head_dim, rows};
+      const cuuint64_t strides[1] = {(cuuint64_t)m.head_dim * 2};
+      const cuuint32_t box[2] = {64, (cuuint32_t)desc->page_size};
+      I->kv2_map = encode_map(I->kv, 2, dims, strides, box);
     }
     I->free_pages.resize(I->n_pages);
     for (int64_t i = 0; i < I->n_pages; ++i) I->free_pages[i] = (int32_t)(I->n_pages - 1 - i);  // pop_back -> 0,1,..
