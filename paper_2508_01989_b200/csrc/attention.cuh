@@ -328,9 +328,9 @@ __global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_
 //   softmax    8 warps, 2 threads per row (TMEM lane): warp w < 4 takes keys 0-63 of rows
 //              32w.., warp w + 4 keys 64-127; the pair exchanges its row max through smem, then
 //              writes bf16 P_j over its own S_j columns in TMEM (two keys per 32-bit column)
-//   MMA warp   O_j = P_j V_j            (A = P from TMEM, B = V MN-major SW128) -> TMEM O[j&1]
-//   softmax    o = o * 2^(m_prev - m_j) + O_j in registers, each thread of a row pair half of the
-//              head dims (one tile behind, off the MMA's path)
+//   MMA warp   O += P_j V_j             (A = P from TMEM, B = V MN-major SW128), O in TMEM
+//   softmax    lazy rescale: O and l move to a new base only when the row max grows by > 2^8
+//              (rare after the first tiles), so the loop never reads O
 // The MMA warp issues S_{j+1} before waiting for P_j, so QK^T of the next tile overlaps the
 // softmax of the current one. K and V tiles stream through separate TMA rings (3 / 2 stages, one
 // 2 KiB box per page and 64-dim half), K_j is released when S_j completes, V_j when O_j does.
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   constexpr int TT = C::TT;
   extern __shared__ uint8_t attn_smem_raw[];
   __shared__ uint64_t q_full, k_full[kPfStages], k_empty[kPfStages], v_full[kPfVStages], v_empty[kPfVStages];
-  __shared__ uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  __shared__ uint64_t s_full[2], p_full[2], o_full[2];
   __shared__ uint32_t tmem_slot;
   const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -390,7 +390,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 256);
       mbar_init(&o_full[b], 1);
-      mbar_init(&o_empty[b], 256);
     }
     mbar_fence_init();
   }
@@ -446,7 +445,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const int st = i % kPfVStages;
       mbar_wait(&p_full[i & 1], (i >> 1) & 1);
       mbar_wait(&v_full[st], (i / kPfVStages) & 1);
-      if (i >= 2) mbar_wait(&o_empty[i & 1], ((i - 2) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t vb = sbase + C::kOffV + st * C::kKBytes;
@@ -454,8 +452,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         // thread overwrites only the S columns it has read itself)
 #pragma unroll
         for (int kk = 0; kk < kPfKeys / 16; ++kk)
-          umma_bf16_tmem_a(tmem + 256 + (i & 1) * 128, tmem + (i & 1) * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
-                           umma_smem_desc_mn128(vb + kk * 2048, C::kSlab, 1024), idesc_o, kk > 0 ? 1u : 0u);
+          umma_bf16_tmem_a(tmem + 256, tmem + (i & 1) * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
+                           umma_smem_desc_mn128(vb + kk * 2048, C::kSlab, 1024), idesc_o, (i | kk) ? 1u : 0u);
         umma_commit(&o_full[i & 1]);
         umma_commit(&v_empty[st]);
       }
@@ -491,78 +489,95 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const int lim = valid ? pos0 + qoff + t + 1 : 0;  // causal: keys < lim
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     float* xmax = reinterpret_cast<float*>(attn_smem_raw + (sbase - smem_u32(attn_smem_raw)) + C::kOffX);  // [2][2][128]
-    float o[HD];
+    // O accumulates in TMEM across tiles relative to a per-row base m_used; the base moves (and
+    // O, l are rescaled) only when the row max exceeds it by more than 2^8, so P <= 256 in bf16.
+    constexpr float kRescale = 8.f;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t s_addr = tmem + lane_off + (j & 1) * 128 + half * 64;
+      const int key0 = j * kPfKeys + half * 64;
+      const bool full = key0 + 63 < lim;  // no causal / length mask inside this thread's 64 keys
+      // this thread's 64 scores stay in registers for both passes (one TMEM round trip)
+      uint32_t v[64];
+      tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      tmem_ld_32x32b_x32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      tmem_ld_wait();
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if (full) {
 #pragma unroll
-    for (int c = 0; c < HD; ++c) o[c] = 0.f;
-    float m = -INFINITY, l = 0.f, m_o = -INFINITY, m_tile0 = 0.f, m_tile1 = 0.f;  // base of P_j, j even / odd
-    // iteration j: softmax of tile j (if any), then fold O_{j-1} into o (one tile behind)
-    for (int j = 0; j <= n_tiles; ++j) {
-      if (j < n_tiles) {
-        mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t s_addr = tmem + lane_off + (j & 1) * 128 + half * 64;
-        const int key0 = j * kPfKeys + half * 64;
-        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(s_addr + c * 32, v);
-          tmem_ld_wait();
-          const int kc = key0 + c * 32;
+        for (int x = 0; x < 64; ++x) mx4[x & 3] = fmaxf(mx4[x & 3], __uint_as_float(v[x]));
+      } else {
 #pragma unroll
-          for (int x = 0; x < 32; ++x)
-            if (kc + x < lim) mx4[x & 3] = fmaxf(mx4[x & 3], __uint_as_float(v[x]));
-        }
-        // pair exchange of the row max (buffer j & 1; the partner reads it before the next barrier)
-        const float mine = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
-        xmax[((j & 1) * 2 + half) * 128 + r] = mine;
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-        const float mx = fmaxf(m, fmaxf(mine, xmax[((j & 1) * 2 + (half ^ 1)) * 128 + r]));
-        const float base = mx == -INFINITY ? 0.f : mx;
-        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(s_addr + c * 32, v);
-          tmem_ld_wait();
-          uint32_t pk[16];
-          const int kc = key0 + c * 32;
-#pragma unroll
-          for (int x = 0; x < 16; ++x) {
-            const float p0 = kc + 2 * x < lim ? fast_exp2(__uint_as_float(v[2 * x]) * p.scale_log2 - base) : 0.f;
-            const float p1 = kc + 2 * x + 1 < lim ? fast_exp2(__uint_as_float(v[2 * x + 1]) * p.scale_log2 - base) : 0.f;
-            sum4[x & 3] += p0 + p1;
-            pk[x] = pack_bf16(p0, p1);
-          }
-          tmem_st_32x32b_x16(s_addr + c * 16, pk);  // P over this thread's already-read S columns
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&p_full[j & 1]);
-        const float sum = (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
-        l = (m == -INFINITY ? 0.f : l * fast_exp2(m - base)) + sum;
-        m = mx;
-        if (j & 1) m_tile1 = base; else m_tile0 = base;
+        for (int x = 0; x < 64; ++x)
+          if (key0 + x < lim) mx4[x & 3] = fmaxf(mx4[x & 3], __uint_as_float(v[x]));
       }
-      if (j >= 1) {
-        const int i = j - 1;
-        mbar_wait(&o_full[i & 1], (i >> 1) & 1);
+      // pair exchange of the row max (buffer j & 1; the partner reads it before the next barrier)
+      const float mine = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
+      xmax[((j & 1) * 2 + half) * 128 + r] = mine;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      const float mx = fmaxf(mine, xmax[((j & 1) * 2 + (half ^ 1)) * 128 + r]);  // tile row max
+      // rescale decision per row; the TMEM traffic is warp-collective (tcgen05.ld/st .sync.aligned),
+      // so a warp rescales when any of its rows needs it (factor 1 for the others)
+      const bool need = mx > m_used + kRescale;  // (also the first valid tile: m_used = -inf)
+      if (j > 0 && __any_sync(0xffffffffu, need && m_used != -INFINITY)) {
+        // O holds PV_0..PV_{j-1}: S_j complete => PV_{j-2} complete (in-order), so PV_{j-1}'s
+        // barrier phase cannot alias
+        const float corr = (need && m_used != -INFINITY) ? fast_exp2(m_used - mx) : 1.f;
+        mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        const float mt = (i & 1) ? m_tile1 : m_tile0;
-        const float corr = m_o == -INFINITY ? 0.f : fast_exp2(m_o - mt);
+        uint32_t ov[HD];
+        const uint32_t o_addr = tmem + lane_off + 256 + half * HD;
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_off + 256 + (i & 1) * 128 + half * HD + c * 32, v);
-          tmem_ld_wait();
+        for (int c = 0; c < HD / 32; ++c)
+          tmem_ld_32x32b_x32(o_addr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
+        tmem_ld_wait();
 #pragma unroll
-          for (int x = 0; x < 32; ++x) o[c * 32 + x] = o[c * 32 + x] * corr + __uint_as_float(v[x]);
-        }
-        m_o = mt;
-        tc_fence_before();
-        mbar_arrive(&o_empty[i & 1]);
+        for (int x = 0; x < HD; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * corr);
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c)
+          tmem_st_32x32b_x16(o_addr + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(&ov[c * 16]));
+        l *= corr;
       }
+      if (need) m_used = mx;
+      const float base = m_used == -INFINITY ? 0.f : m_used;
+      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[32];
+      if (full) {
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base));
+          sum4[x & 3] += p0 + p1;
+          pk[x] = pack_bf16(p0, p1);
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          const float p0 = key0 + 2 * x < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base)) : 0.f;
+          const float p1 =
+              key0 + 2 * x + 1 < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base)) : 0.f;
+          sum4[x & 3] += p0 + p1;
+          pk[x] = pack_bf16(p0, p1);
+        }
+      }
+      // P over this thread's already-read S columns
+      tmem_st_32x32b_x16(s_addr, *reinterpret_cast<const uint32_t(*)[16]>(&pk[0]));
+      tmem_st_32x32b_x16(s_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(&pk[16]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[j & 1]);
+      l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
     }
+    // O final once the last PV completes (S_{n-1} complete => PV_{n-3} complete)
+    mbar_wait(&o_full[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    tc_fence_after();
+    uint32_t o[HD];
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c)
+      tmem_ld_32x32b_x32(tmem + lane_off + 256 + half * HD + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+    tmem_ld_wait();
     // row sum = both halves' partial sums (same base)
     xmax[half * 128 + r] = l;
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
@@ -573,10 +588,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 #pragma unroll
       for (int c = 0; c < HD / 8; ++c) {
         uint4 w;
-        w.x = pack_bf16(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-        w.y = pack_bf16(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-        w.z = pack_bf16(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-        w.w = pack_bf16(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+        w.x = pack_bf16(__uint_as_float(o[c * 8 + 0]) * inv, __uint_as_float(o[c * 8 + 1]) * inv);
+        w.y = pack_bf16(__uint_as_float(o[c * 8 + 2]) * inv, __uint_as_float(o[c * 8 + 3]) * inv);
+        w.z = pack_bf16(__uint_as_float(o[c * 8 + 4]) * inv, __uint_as_float(o[c * 8 + 5]) * inv);
+        w.w = pack_bf16(__uint_as_float(o[c * 8 + 6]) * inv, __uint_as_float(o[c * 8 + 7]) * inv);
         st_global_v4(dst + c * 8, w);
       }
     }
