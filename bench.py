@@ -118,6 +118,36 @@ def cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=1):
             "seconds_per_step": sec, **det}
 
 
+def migration_bench(src, model, dev, hbm_gbs, n_tokens=(1024, 4096), reps=8):
+    """KV migration: tc_kv_migrate of a request's first n_tokens rows
+    between two instances, timed by the library with CUDA events around the page-copy kernel.
+    This box exposes one GPU, so both instances sit on it (weights shared) and the copy is an
+    HBM read + write of whole 2 MiB pages; across GPUs the same kernel pushes over NVLink."""
+    from paper_2508_01989_b200 import Instance
+    dst = Instance(model, device=dev, weight_seed=1, kv_pool_tokens=max(n_tokens) + 1024, max_step_tokens=512,
+                   max_seqs=8, max_context=max(n_tokens) + 64, share_weights=src)
+    out = []
+    rid = 1 << 40
+    for n in n_tokens:
+        src.kv_reserve(rid, n)
+        a, b = src, dst
+        ms, nbytes = [], 0
+        for i in range(reps + 2):
+            a.migrate_to(b, rid, n)
+            t, nbytes = a.migrate_wait()
+            if i >= 2:
+                ms.append(t)
+            a, b = b, a
+        a.kv_release(rid)
+        t = statistics.median(ms)
+        out.append({"tokens": n, "bytes": nbytes, "ms": t, "copy_gb_s": nbytes / t / 1e6,
+                    "hbm_gb_s": 2 * nbytes / t / 1e6, "hbm_frac": 2 * nbytes / t / 1e6 / hbm_gbs})
+    dst.close()
+    return {"kernel": "kv_copy_pages (whole 2 MiB pages, 16 B vectors)", "path": "same-GPU pool-to-pool copy "
+            "(1-GPU box): bound = HBM read+write; cross-GPU it is an NVLink P2P push (target 900 GB/s, not "
+            "measurable on one GPU)", "median_of": reps, "sizes": out}
+
+
 def reduce_max(vals, device=None):
     """Max over ranks of a list of floats (timing rule: multi-GPU numbers are the max over ranks)."""
     import torch
@@ -224,8 +254,8 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
-    inst = Instance(args.model, device=dev, weight_seed=1, kv_pool_tokens=(D + 2) * (ctx + 64) + prefix + P + 4096,
-                    max_step_tokens=max(P + D, 512), max_seqs=D + 8, max_context=max(ctx, prefix + P) + 64)
+    inst = Instance(args.model, device=dev, weight_seed=1, kv_pool_tokens=(D + 2) * (ctx + 64) + prefix + P + 8192,
+                    max_step_tokens=max(P + D, 512), max_seqs=D + 8, max_context=max(ctx, prefix + P, 4096) + 64)
     dims = inst.dims.as_dict()
     V = dims["vocab"]
     import numpy as np
@@ -313,6 +343,8 @@ def main():
                                      "bound_ms": 1e3 * max(v["flops"] / (peak_sus * 1e12), v["bytes"] / (hbm * 1e9)),
                                      "measured_ms": phases.get(k)} for k, v in cost.items()}}
 
+    migration = migration_bench(inst, args.model, dev, hbm)
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=1)
@@ -327,7 +359,7 @@ def main():
                                      "weight_stream_bound_ms": 1e3 * sum(c["bytes"] for k, c in
                                                                          step_cost(dims, 0, 0, D, ctx, D).items()) /
                                                                (measured_peaks()[0] * 1e9)},
-                "cpu_baseline": cb}
+                "migration": migration, "cpu_baseline": cb}
         print(json.dumps(line))
     inst.close()
     if world > 1:

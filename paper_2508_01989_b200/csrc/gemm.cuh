@@ -54,6 +54,7 @@ struct QkvRopeArgs {
   const float2* rope_cs;   // [position][head_dim / 2] (cos, sin)
   const int* positions;    // [rows]
   const int* row_seq;      // [rows] sequence of the row
+  const int* row_kv;       // [rows] KV pool row of the token: page * page_size + slot
   const int* seq_bt_off;   // [seqs] offset into block_tables
   const int* block_tables;
   long long page_stride;   // elements per page
@@ -80,6 +81,8 @@ struct GemmArgs {
   QkvRopeArgs rope;          // EPI_QKV_ROPE only
   float* red_out;            // small-M streaming mode: every unit red.adds its partial into this
                              // zeroed fp32 [M, N] scratch; a finish kernel applies the epilogue
+  int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
+  int stages;                // gemm_ws_2sm: smem ring depth for this token tile
 };
 
 template <int BN>

@@ -1,0 +1,342 @@
+// Weight-stationary pair GEMM for the mixed hybrid step, C = X * W^T
+// computed transposed: the MMA's M dimension runs over WEIGHT rows and its N dimension over
+// the step's TOKENS.
+//
+// Why: a step packs T = prefill chunk + decodes rows (576 at the bench config). With tokens
+// on M the 128-row tile pads 576 to 640 (11% dead MMA work) and the 256-row pair tile pads it
+// to 768. UMMA N, in contrast, is any multiple of 16 up to 256, so the token tile is sized to
+// the step: n_tt = ceil(T / 256) tiles of TN = round_up(T / n_tt, 32) tokens (576 -> 3 x 192,
+// 512 -> 2 x 256, 1100 -> 5 x 224), padding at most 31 rows per tile.
+//
+// CTA pair (cluster 2x1, tcgen05.mma.cta_group::2, M = 256, N = TN, K = 16): each CTA stages
+// its own 128 weight rows (16 KB per 64-deep k-block) and HALF of the token tile (TN/2 rows),
+// so a 256 x 192 pair tile costs each SM 28 KB of L2->SMEM traffic per k-block for 384 MMA
+// cycles (73 B/clk) against 96 B/clk for the 128 x 256 single-SM tile. The leader issues the
+// MMAs; both CTAs' TMA credit the leader's full barrier; commits multicast to both CTAs.
+//
+// Unit order: token tile fastest, so the n_tt pairs that share a weight tile run together and
+// the 15 GB weight stream leaves DRAM once (the activations, <= 17 MB, stay in L2).
+//
+// Epilogue (warps 4-7): TMEM holds [128 weight rows (lanes)] x [TN tokens (columns)]. Each
+// 32-token chunk is read with tcgen05.ld 32x32b (thread = weight row), transposed through a
+// double-buffered, XOR-swizzled fp32 staging tile (bank-conflict-free both ways), and then
+// processed token-row-wise: thread (token t, segment s) owns 32 consecutive features of one
+// token, which is what every fused op needs (bias, SwiGLU on 64-row interleaved gate/up
+// blocks, RoPE pairs (j, j + head_dim/2) inside one head, paged KV append, fp32 residual add;
+// split-K partials of the residual GEMMs are reduced with red.global.add.v4.f32).
+#pragma once
+
+#include "gemm.cuh"
+
+namespace tc {
+
+constexpr int kWsMaxStages = 8;
+constexpr int kWsWBytes = 128 * kGemmBK * 2;           // this CTA's 128 weight rows per k-block
+constexpr int kWsStagingFloats = 32 * 128;             // one 32-token x 128-feature fp32 chunk
+constexpr int kWsSmemBytes = 232448;                   // max dynamic shared memory per CTA (sm_100)
+constexpr int kWsBarBytes = 256;
+constexpr int kWsRingBudget = kWsSmemBytes - 1024 - 2 * kWsStagingFloats * 4 - kWsBarBytes;
+
+__host__ __device__ constexpr int ws_stage_bytes(int tn) { return kWsWBytes + (tn / 2) * kGemmBK * 2; }
+__host__ __device__ constexpr int ws_stages(int tn) {
+  return ws_stage_bytes(tn) * kWsMaxStages <= kWsRingBudget ? kWsMaxStages : kWsRingBudget / ws_stage_bytes(tn);
+}
+
+// Features [4ch, 4ch + 4) of staged token row t (XOR swizzle: conflict-free transposed writes
+// by 32 weight rows and row-wise float4 reads by (2 tokens x 4 segments) quarter-warps).
+__device__ __forceinline__ int ws_stg_idx(int t, int ch) { return t * 128 + ((ch ^ ((ch >> 3) & 3) ^ ((t & 1) << 2)) << 2); }
+__device__ __forceinline__ float4 ws_ld4(const float* sb, int t, int ch) {
+  return *reinterpret_cast<const float4*>(sb + ws_stg_idx(t, ch));
+}
+
+// Token-row epilogue: token tok (valid), 32 features of segment s of the CTA's 128 weight rows
+// starting at global weight row fbase.
+template <int EPI>
+__device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const float* sb, int t, int s, int tok, int fbase,
+                                                int pos, int kv_row) {
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_BIAS) {
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)tok * args.ldo + fbase + s * 32;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 a = ws_ld4(sb, t, s * 8 + 2 * q), b = ws_ld4(sb, t, s * 8 + 2 * q + 1);
+      if constexpr (EPI == EPI_BF16_BIAS) {
+        const __nv_bfloat16* bb = args.bias + fbase + s * 32 + q * 8;
+        a.x += __bfloat162float(bb[0]); a.y += __bfloat162float(bb[1]);
+        a.z += __bfloat162float(bb[2]); a.w += __bfloat162float(bb[3]);
+        b.x += __bfloat162float(bb[4]); b.y += __bfloat162float(bb[5]);
+        b.z += __bfloat162float(bb[6]); b.w += __bfloat162float(bb[7]);
+      }
+      st_global_v4(out + q * 8, make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w)));
+    }
+  } else if constexpr (EPI == EPI_F32) {
+    float* out = reinterpret_cast<float*>(args.out) + (size_t)tok * args.ldo + fbase + s * 32;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 a = ws_ld4(sb, t, s * 8 + q);
+      st_global_v4(out + q * 4, make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(a.w)));
+    }
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    float* out = reinterpret_cast<float*>(args.out) + (size_t)tok * args.ldo + fbase + s * 32;
+    if (args.splits > 1) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 a = ws_ld4(sb, t, s * 8 + q);
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(out + q * 4), "f"(a.x), "f"(a.y), "f"(a.z),
+                     "f"(a.w)
+                     : "memory");
+      }
+    } else {
+      float4 x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = *reinterpret_cast<const float4*>(out + q * 4);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 a = ws_ld4(sb, t, s * 8 + q);
+        x[q].x += a.x; x[q].y += a.y; x[q].z += a.z; x[q].w += a.w;
+        *reinterpret_cast<float4*>(out + q * 4) = x[q];
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    // weight rows [fbase, fbase + 64) = gate, [fbase + 64, fbase + 128) = up of outputs fbase / 2 + [0, 64)
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)tok * args.ldo + fbase / 2 + s * 16;
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 g = ws_ld4(sb, t, s * 4 + q), u = ws_ld4(sb, t, 16 + s * 4 + q);
+      w[q * 2] = pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y);
+      w[q * 2 + 1] = pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w);
+    }
+    st_global_v4(out, make_uint4(w[0], w[1], w[2], w[3]));
+    st_global_v4(out + 8, make_uint4(w[4], w[5], w[6], w[7]));
+  } else if constexpr (EPI == EPI_QKV_ROPE) {
+    // this thread: rotation pairs (j, j + DH/2), j in [j0, j0 + 16), of head fbase / DH + hh
+    const QkvRopeArgs& r = args.rope;
+    const int DH = r.head_dim, half = DH >> 1;
+    const int hh = (s * 16) / half, j0 = (s * 16) % half;
+    const int head = fbase / DH + hh;
+    const int lo_f = hh * DH + j0;  // tile-local feature of the first lo element
+    const bool is_q = head < r.n_heads, is_k = !is_q && head < r.n_heads + r.n_kv_heads;
+    __nv_bfloat16* dst;
+    if (is_q) {
+      dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)tok * args.ldo + head * DH;
+    } else {
+      const int page = kv_row / r.page_size, slot = kv_row - page * r.page_size;
+      const int kvh = head - r.n_heads - (is_k ? 0 : r.n_kv_heads);
+      dst = r.kv + (size_t)page * r.page_stride +
+            ((((size_t)r.layer * r.n_kv_heads + kvh) * 2 + (is_k ? 0 : 1)) * r.page_size + slot) * DH;
+    }
+    float lo[16], hi[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 a = ws_ld4(sb, t, (lo_f >> 2) + q), b = ws_ld4(sb, t, ((lo_f + half) >> 2) + q);
+      lo[q * 4] = a.x; lo[q * 4 + 1] = a.y; lo[q * 4 + 2] = a.z; lo[q * 4 + 3] = a.w;
+      hi[q * 4] = b.x; hi[q * 4 + 1] = b.y; hi[q * 4 + 2] = b.z; hi[q * 4 + 3] = b.w;
+    }
+    if (args.bias) {
+      const __nv_bfloat16* bl = args.bias + fbase + lo_f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        lo[i] += __bfloat162float(bl[i]);
+        hi[i] += __bfloat162float(bl[half + i]);
+      }
+    }
+    if (is_q || is_k) {
+      const float2* cs = r.rope_cs + (size_t)pos * half + j0;
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const float4 c = *reinterpret_cast<const float4*>(cs + i);  // (cos, sin) x 2
+        const float a0 = lo[i], b0 = hi[i], a1 = lo[i + 1], b1 = hi[i + 1];
+        lo[i] = a0 * c.x - b0 * c.y;
+        hi[i] = b0 * c.x + a0 * c.y;
+        lo[i + 1] = a1 * c.z - b1 * c.w;
+        hi[i + 1] = b1 * c.z + a1 * c.w;
+      }
+    }
+    uint32_t wl[8], wh[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      wl[i] = pack_bf16(lo[2 * i], lo[2 * i + 1]);
+      wh[i] = pack_bf16(hi[2 * i], hi[2 * i + 1]);
+    }
+    st_global_v4(dst + j0, make_uint4(wl[0], wl[1], wl[2], wl[3]));
+    st_global_v4(dst + j0 + 8, make_uint4(wl[4], wl[5], wl[6], wl[7]));
+    st_global_v4(dst + half + j0, make_uint4(wh[0], wh[1], wh[2], wh[3]));
+    st_global_v4(dst + half + j0 + 8, make_uint4(wh[4], wh[5], wh[6], wh[7]));
+  }
+}
+
+// map_w: weights [N, K], box 64 x 128 rows; map_x: activations [rows, K], box 64 x TN/2 rows;
+// map_o (EPI_RESID_F32 only): the fp32 residual [rows, N], box 128 features x 32 tokens, no
+// swizzle -- each 32-token chunk is staged densely and added by one TMA bulk reduction
+// (cp.reduce.async.bulk.tensor .add), which also reduces the split-K partials.
+// args.m_tiles = token tiles, args.n_tiles = 256-row weight pair tiles, args.tn, args.stages.
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_ws_2sm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                const __grid_constant__ CUtensorMap map_o, GemmArgs args) {
+  const int TN = args.tn, S = args.stages;
+  const int stage_bytes = ws_stage_bytes(TN);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg = reinterpret_cast<float*>(smem + S * stage_bytes);  // [2][32][128]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + 2 * kWsStagingFloats);
+  uint64_t* empty_bar = full_bar + kWsMaxStages;
+  uint64_t* tfull_bar = empty_bar + kWsMaxStages;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;            // [2] (leader's copy is used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_w);
+    tma_prefetch_desc(&map_x);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    mbar_fence_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int half_tn = TN / 2;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < args.units; u += n_pairs) {
+        const Unit w = unit_of(args, u);  // w.mt = token tile, w.nt = weight pair tile
+        for (int kb = w.k0; kb < w.k1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_bytes);
+          uint8_t* st = smem + stage * stage_bytes;
+          tma_load_2d_2sm(st, &map_w, &full_bar[stage], kb * kGemmBK, w.nt * 256 + (int)rank * 128, kEvictNormal);
+          tma_load_2d_2sm(st + kWsWBytes, &map_x, &full_bar[stage], kb * kGemmBK, w.mt * TN + (int)rank * half_tn,
+                          kEvictLast);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      const uint32_t idesc = umma_idesc_bf16(256, TN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int u = pair; u < args.units; u += n_pairs) {
+        const Unit w = unit_of(args, u);
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        ++local;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = w.k0; kb < w.k1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t w_addr = smem_u32(smem + stage * stage_bytes);
+            const uint32_t x_addr = w_addr + kWsWBytes;
+#pragma unroll
+            for (int k = 0; k < kGemmBK / 16; ++k)
+              umma_bf16_2sm(d_tmem, umma_smem_desc<kGemmBK * 2>(w_addr + k * 32),
+                            umma_smem_desc<kGemmBK * 2>(x_addr + k * 32), idesc, (kb > w.k0 || k > 0) ? 1u : 0u);
+            umma_commit_2sm_multicast(&empty_bar[stage]);
+            if (kb == w.k1 - 1) umma_commit_2sm_multicast(&tfull_bar[acc]);
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;              // TMEM lane quarter
+    const int f = ew * 32 + lane;         // weight row within this CTA's 128 (transposed write)
+    const int et = threadIdx.x - 128;     // 0..127
+    const int t = et >> 2, s = et & 3;    // token row / 32-feature segment (row phase)
+    const int fch = f >> 2, fe = f & 3;
+    int local = 0, chunk_ctr = 0;
+    for (int u = pair; u < args.units; u += n_pairs) {
+      const Unit w = unit_of(args, u);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      ++local;
+      // per-token RoPE / KV-append metadata of this thread's rows, fetched while the MMAs run
+      int pos_pf[8], kv_pf[8];
+      if constexpr (EPI == EPI_QKV_ROPE) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int tok = w.mt * TN + c * 32 + t;
+          const bool ok = c * 32 < TN && tok < args.M;
+          pos_pf[c] = ok ? __ldg(args.rope.positions + tok) : 0;
+          kv_pf[c] = ok ? __ldg(args.rope.row_kv + tok) : 0;
+        }
+      }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int fbase = w.nt * 256 + (int)rank * 128;
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
+#pragma unroll
+      for (int ci = 0; ci < 8; ++ci) {
+        const int c0 = ci * 32;
+        if (c0 >= TN) break;
+        ++chunk_ctr;
+        float* sb = stg + (chunk_ctr & 1) * kWsStagingFloats;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        tmem_ld_wait();
+        if (c0 + 32 >= TN) {  // accumulator fully read: release it to the MMA warp early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
+        }
+        if constexpr (EPI == EPI_RESID_F32) {
+          // dense [32 tokens][128 features] chunk -> one TMA bulk add into the residual; the
+          // issuing thread first makes sure the reduction that last read this buffer is done
+          if (et == 0) bulk_wait_group_read<1>();
+          epi_bar();
+          const int tok0 = w.mt * TN + c0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sb[i * 128 + f] = tok0 + i < args.M ? __uint_as_float(r[i]) : 0.f;
+          fence_async_smem();
+          epi_bar();
+          if (et == 0) {
+            tma_reduce_add_2d(&map_o, smem_u32(sb), fbase, tok0);
+            bulk_commit_group();
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sb[ws_stg_idx(i, fch) + fe] = __uint_as_float(r[i]);
+          epi_bar();
+          const int tok = w.mt * TN + c0 + t;
+          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, pos_pf[ci], kv_pf[ci]);
+        }
+      }
+    }
+  }
+
+  if (EPI == EPI_RESID_F32 && threadIdx.x == 128) bulk_wait_group<0>();  // residual updates landed
+  tc_fence_before();
+  cluster_sync();  // every MMA retired and both epilogues drained before TMEM is released
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
+}  // namespace tc

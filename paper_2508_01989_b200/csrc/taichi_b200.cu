@@ -11,6 +11,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -25,6 +27,7 @@
 #include "common.cuh"
 #include "elementwise.cuh"
 #include "gemm.cuh"
+#include "gemm_ws.cuh"
 #include "taichi_b200.h"
 
 namespace {
@@ -102,6 +105,21 @@ CUtensorMap make_kmajor_map(const void* base, uint64_t rows, uint64_t cols, uint
   return m;
 }
 
+// fp32 [rows, cols] row-major, box 128 cols x 32 rows, no swizzle: the target of the
+// weight-stationary GEMM's TMA bulk residual add (one 32-token x 128-feature chunk per box).
+CUtensorMap make_resid_map(void* base, uint64_t rows, uint64_t cols) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 4};
+  const cuuint32_t box[2] = {128, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TcFail{TC_ERR_CUDA, "cuTensorMapEncodeTiled (resid) failed: " + std::to_string((int)r)};
+  return m;
+}
+
 CUtensorMap encode_map(void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
   CUtensorMap m;
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -139,6 +157,12 @@ void init_kernel_attrs(int dev) {
   DeviceGuard g(dev);
   set_gemm_smem<128, 0>(); set_gemm_smem<128, 1>(); set_gemm_smem<128, 2>(); set_gemm_smem<128, 3>(); set_gemm_smem<128, 4>(); set_gemm_smem<128, 5>();
   set_gemm_smem<256, 0>(); set_gemm_smem<256, 1>(); set_gemm_smem<256, 2>(); set_gemm_smem<256, 3>(); set_gemm_smem<256, 4>(); set_gemm_smem<256, 5>();
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
+  TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
   // attention kernels run 2 CTAs/SM (~97 KB each): ask for the maximum shared-memory carveout,
   // otherwise the driver's default split leaves room for only one (ncu: occupancy 7.8%)
   TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
@@ -262,6 +286,32 @@ struct WMat {
   const CUtensorMap& map(int bn) const { return bn == 128 ? map128 : map256; }
 };
 
+// Activation operand [rows, cols] of the projections: the 128-row map of the token-major
+// kernels plus lazily encoded maps with box heights 16..128 (half token tiles of gemm_ws_2sm).
+struct ActMap {
+  const void* base = nullptr;
+  uint64_t rows = 0, cols = 0;
+  CUtensorMap m128;
+  std::array<CUtensorMap, 9> by16;
+  std::array<bool, 9> have{};
+  void init(const void* p, uint64_t r, uint64_t c) {
+    base = p;
+    rows = r;
+    cols = c;
+    m128 = make_kmajor_map(p, r, c, 128);
+    have.fill(false);
+  }
+  const CUtensorMap& box(int box_rows) {
+    TC_REQUIRE(box_rows % 16 == 0 && box_rows >= 16 && box_rows <= 128, "gemm: bad activation box");
+    const int i = box_rows / 16;
+    if (!have[i]) {
+      by16[i] = make_kmajor_map(base, rows, cols, (uint32_t)box_rows);
+      have[i] = true;
+    }
+    return by16[i];
+  }
+};
+
 struct SkWorkspace {
   float* ws = nullptr;
   int* cnt = nullptr;
@@ -284,15 +334,100 @@ void launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb128, const tc::
   }
 }
 
-// out = epi(A[M,K] * W[N,K]^T). a_map: box 128 rows over the activation buffer.
-int run_gemm(const CUtensorMap& a_map, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
+// Weight-stationary pair kernel (gemm_ws.cuh) for mixed / prefill steps: T > kWsMinRows rows,
+// weight rows a multiple of 256. TC_GEMM_WS=0 in the environment falls back to the token-major
+// kernels (A/B switch for measurement).
+constexpr int kWsMinRows = 128;
+bool ws_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TC_GEMM_WS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensorMap& mo, const tc::GemmArgs& args,
+                    int epi, int grid, cudaStream_t s) {
+  const int smem = tc::kWsSmemBytes;
+  switch (epi) {
+    case tc::EPI_BF16: tc::gemm_ws_2sm<tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    case tc::EPI_BF16_BIAS: tc::gemm_ws_2sm<tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    case tc::EPI_RESID_F32: tc::gemm_ws_2sm<tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    case tc::EPI_SWIGLU: tc::gemm_ws_2sm<tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    case tc::EPI_F32: tc::gemm_ws_2sm<tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    case tc::EPI_QKV_ROPE: tc::gemm_ws_2sm<tc::EPI_QKV_ROPE><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
+  }
+}
+
+int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi, int sms,
+                cudaStream_t s, int force_splits, const tc::QkvRopeArgs* rope, const CUtensorMap* out_map) {
+  const int N = (int)w.rows, K = (int)w.cols;
+  TC_REQUIRE(N % 256 == 0, "gemm_ws: weight rows must be a multiple of 256");
+  tc::GemmArgs args{};
+  const int n_tt = (M + 255) / 256;
+  args.tn = ((M + n_tt - 1) / n_tt + 31) / 32 * 32;
+  args.stages = tc::ws_stages(args.tn);
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.m_tiles = n_tt;
+  args.n_tiles = N / 256;
+  args.kb = K / tc::kGemmBK;
+  const long long tiles = (long long)args.m_tiles * args.n_tiles;
+  const int pairs = sms / 2;
+  int sp = 1;
+  if (epi == tc::EPI_RESID_F32) {
+    if (force_splits > 0) {
+      sp = force_splits;
+    } else if (tiles < pairs) {
+      // red.add split-K: minimise waves * (k-blocks per split + per-unit overhead of ~8 k-blocks)
+      double best = 1e30;
+      for (int cand = 1; cand <= std::min(16, std::max(1, args.kb / 4)); ++cand) {
+        const long long waves = (tiles * cand + pairs - 1) / pairs;
+        const double t = (double)waves * ((args.kb + cand - 1) / cand + 8);
+        if (t < best - 1e-9) {
+          best = t;
+          sp = cand;
+        }
+      }
+    }
+  }
+  args.splits = std::max(1, std::min(sp, args.kb));
+  args.units = (int)(tiles * args.splits);
+  args.out = out;
+  args.ldo = ldo;
+  args.bias = bias;
+  if (epi == tc::EPI_QKV_ROPE) {
+    TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
+    TC_REQUIRE(128 % rope->head_dim == 0, "gemm_ws: a 128-row half tile must cover whole heads");
+    args.rope = *rope;
+  }
+  const int grid = 2 * (int)std::min<long long>(pairs, args.units);
+  CUtensorMap resid_map;
+  if (epi == tc::EPI_RESID_F32) {
+    // the residual's TMA map: the instance's (built once) or, for tc_gemm, one over `out`
+    TC_REQUIRE(ldo == N, "gemm_ws: residual output must be dense [M, N]");
+    resid_map = out_map ? *out_map : make_resid_map(out, (uint64_t)M, (uint64_t)N);
+  }
+  launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), args, epi, grid, s);
+  TC_CUDA(cudaGetLastError());
+  return 1;
+}
+
+// out = epi(A[M,K] * W[N,K]^T). a: the activation buffer's maps.
+int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
              int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
-             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr) {
+             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr, const CUtensorMap* out_map = nullptr) {
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(K % 64 == 0, "gemm: K must be a multiple of 64");
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
-  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256 || force_bn == 512,
-             "gemm: tile width must be 128, 256 or 512 (= 2-SM 256 x 256)");
+  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256 || force_bn == 512 || force_bn == 1024,
+             "gemm: tile width must be 128, 256, 512 (= 2-SM 256 x 256) or 1024 (= weight-stationary pair)");
+  if (red_out == nullptr && N % 256 == 0 &&
+      (force_bn == 1024 || (force_bn == 0 && ws_enabled() && M > kWsMinRows && epi != tc::EPI_F32)))
+    return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map);
+  const CUtensorMap& a_map = a.m128;
   const bool two_sm = N % 256 == 0 && (force_bn == 512 || (force_bn == 0 && M > kGemm2MinM));
   if (two_sm) {
     // pair tiles of 256 rows; splits only through red.add (residual / streaming epilogues)
@@ -426,7 +561,8 @@ struct tc_instance {
   float* logits = nullptr;
   int* ids_dev = nullptr;
   int* ids_host = nullptr;
-  CUtensorMap map_xnorm, map_attn, map_act, map_lm_in;
+  ActMap map_xnorm, map_attn, map_act, map_lm_in;
+  CUtensorMap map_resid;  // fp32 residual stream, target of the GEMMs' TMA bulk adds
   SkWorkspace sk;
   float* stream_scr = nullptr;  // fp32 [<=128, max(qkv_n, 2F)] accumulation scratch (decode-only steps)
   float *attn_ws_o = nullptr, *attn_ws_ml = nullptr;
@@ -571,10 +707,11 @@ void alloc_buffers(tc_instance* I) {
   TC_CUDA(cudaMemset(I->attn_out, 0, (size_t)Tp * m.n_heads * m.head_dim * 2));
   TC_CUDA(cudaMemset(I->act, 0, (size_t)Tp * m.ffn_dim * 2));
   TC_CUDA(cudaMemset(I->lm_in, 0, (size_t)Sp * dm * 2));
-  I->map_xnorm = make_kmajor_map(I->xnorm, Tp, dm, 128);
-  I->map_attn = make_kmajor_map(I->attn_out, Tp, (uint64_t)m.n_heads * m.head_dim, 128);
-  I->map_act = make_kmajor_map(I->act, Tp, m.ffn_dim, 128);
-  I->map_lm_in = make_kmajor_map(I->lm_in, Sp, dm, 128);
+  I->map_xnorm.init(I->xnorm, Tp, dm);
+  I->map_resid = make_resid_map(I->resid, Tp, dm);
+  I->map_attn.init(I->attn_out, Tp, (uint64_t)m.n_heads * m.head_dim);
+  I->map_act.init(I->act, Tp, m.ffn_dim);
+  I->map_lm_in.init(I->lm_in, Sp, dm);
   {
     const int G = m.n_heads / m.n_kv_heads;
     const cuuint64_t dims[3] = {(cuuint64_t)m.head_dim, (cuuint64_t)m.n_heads, (cuuint64_t)Tp};
@@ -605,9 +742,9 @@ void alloc_buffers(tc_instance* I) {
     }
   TC_CUDA(cudaMalloc(&I->rope, cs.size() * sizeof(float2)));
   TC_CUDA(cudaMemcpy(I->rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  // metadata: 3T + 4S + qblocks(<= T + S) * 2 + S (dec) + S (logit rows) + block tables
+  // metadata: 4T + 4S + qblocks(<= T + S) * 2 + S (dec) + S (logit rows) + block tables
   const int64_t max_pages_per_seq = (I->desc.max_context + I->desc.page_size - 1) / I->desc.page_size;
-  I->meta_ints = 3 * (size_t)T + 4 * (size_t)S + 2 * (size_t)(T + S) + 4 * (size_t)S +
+  I->meta_ints = 4 * (size_t)T + 4 * (size_t)S + 2 * (size_t)(T + S) + 4 * (size_t)S +
                  12 * (size_t)S * m.n_kv_heads + 4 * 1024 + 1024 + (size_t)S * max_pages_per_seq + 128;
   TC_CUDA(cudaMallocHost(&I->meta_host, I->meta_ints * 4));
   TC_CUDA(cudaMalloc(&I->meta_dev, I->meta_ints * 4));
@@ -739,7 +876,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     off += (n + 3) & ~size_t(3);
     return o;
   };
-  const size_t o_tok = take(T), o_pos = take(T), o_rseq = take(T), o_qs = take(n_seq), o_ql = take(n_seq),
+  const size_t o_tok = take(T), o_pos = take(T), o_rseq = take(T), o_kvrow = take(T), o_qs = take(n_seq), o_ql = take(n_seq),
                o_p0 = take(n_seq), o_bo = take(n_seq), o_qbs = take(n_qblk), o_qbo = take(n_qblk),
                o_lrow = take(n_logit), o_bt = take(n_bt), o_sega = take(4 * (size_t)n_seg), o_segb = take(4 * (size_t)n_seg),
                o_ent = take(4 * (size_t)max_entries), o_ctaoff = take((size_t)dec_grid + 1);
@@ -760,6 +897,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       h[o_tok + row + k] = tok;
       h[o_pos + row + k] = sl.pos0 + k;
       h[o_rseq + row + k] = i;
+      h[o_kvrow + row + k] = pages[(sl.pos0 + k) / ps] * ps + (sl.pos0 + k) % ps;
     }
     for (int q = 0; q < sl.n_tokens; q += tpc) {
       h[o_qbs + qb] = i;
@@ -783,6 +921,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     h[o_tok + row] = di.token_id;
     h[o_pos + row] = di.pos;
     h[o_rseq + row] = s;
+    h[o_kvrow + row] = pages[di.pos / ps] * ps + di.pos % ps;
     h[o_lrow + lr++] = row;
     ++row;
   }
@@ -877,6 +1016,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   rp.rope_cs = I->rope;
   rp.positions = dm + o_pos;
   rp.row_seq = dm + o_rseq;
+  rp.row_kv = dm + o_kvrow;
   rp.seq_bt_off = dm + o_bo;
   rp.block_tables = dm + o_bt;
   rp.page_stride = I->page_elems;
@@ -919,7 +1059,8 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_o");
-      I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s);
+      I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
+                              nullptr, nullptr, &I->map_resid);
     }
     {
       ProfScope p_(I, "norm");
@@ -940,7 +1081,8 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_down");
-      I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s);
+      I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
+                              nullptr, nullptr, &I->map_resid);
     }
   }
   if (n_logit > 0) {
@@ -1278,7 +1420,8 @@ tc_status tc_gemm(int32_t device, const void* a, const void* b, void* out, const
     w.rows = n;
     w.cols = k;
     w.make_maps();
-    const CUtensorMap am = make_kmajor_map(a, m, k, 128);
+    ActMap am;
+    am.init(a, m, k);
     const int ldo = epilogue == tc::EPI_SWIGLU ? n / 2 : n;
     // one persistent split-K workspace per device (the tile counters self-reset: the last
     // arriver of every split tile zeroes its counter), so calls on one stream reuse it

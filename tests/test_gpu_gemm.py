@@ -125,3 +125,52 @@ def test_gemm_2sm_swiglu_bias_f32(cuda_ok):
     b3 = torch.randn(128256, k, device="cuda", dtype=torch.bfloat16) * 0.03
     _run(a[:65].contiguous(), b3, o3, 65, 128256, k, EPI_F32, bn=512)
     _close(o3, a[:65].float() @ b3.float().T, False)
+
+
+# ---- weight-stationary pair variant (gemm_ws.cuh: tokens on the MMA's N), forced with bn=1024;
+# the token tile TN = round_up(T / ceil(T / 256), 32) covers ragged T (1, 20, 100, 300, 1100 ...)
+@pytest.mark.parametrize("m,n,k", [(576, 6144, 4096), (1, 256, 128), (20, 512, 256), (100, 512, 1024),
+                                   (300, 768, 512), (512, 1024, 4096), (1100, 1024, 4096), (3000, 512, 256),
+                                   (256, 256, 64), (129, 7168, 5120)])
+def test_gemm_ws_bf16(cuda_ok, m, n, k):
+    g = torch.Generator(device="cuda").manual_seed(m * 13 + n + k)
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16, generator=g)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16, generator=g)
+    out = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
+    _run(a, b, out, m, n, k, EPI_BF16, bn=1024)
+    _close(out, a.float() @ b.float().T, True)
+
+
+@pytest.mark.parametrize("m,n,k,splits", [(576, 4096, 14336, 0), (576, 4096, 4096, 3), (576, 4096, 4096, 1),
+                                          (64, 4096, 4096, 0), (333, 5120, 13824, 0), (7, 256, 512, 2)])
+def test_gemm_ws_residual(cuda_ok, m, n, k, splits):
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.02
+    resid = torch.randn(m, n, device="cuda", dtype=torch.float32)
+    ref = resid + a.float() @ b.float().T
+    _run(a, b, resid, m, n, k, EPI_RESID, bn=1024, splits=splits)
+    _close(resid, ref, False)
+
+
+@pytest.mark.parametrize("m,f,k", [(576, 14336, 4096), (97, 512, 256), (1100, 1024, 512)])
+def test_gemm_ws_swiglu(cuda_ok, m, f, k):
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    wg = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
+    wu = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
+    phys = torch.stack([wg.view(f // 64, 64, k), wu.view(f // 64, 64, k)], dim=1).reshape(2 * f, k).contiguous()
+    out = torch.zeros(m, f, device="cuda", dtype=torch.bfloat16)
+    _run(a, phys, out, m, 2 * f, k, EPI_SWIGLU, bn=1024)
+    _close(out, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T), True)
+
+
+def test_gemm_ws_bias_f32(cuda_ok):
+    m, n, k = 300, 7168, 5120
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.05
+    bias = torch.randn(n, device="cuda", dtype=torch.bfloat16)
+    o = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
+    _run(a, b, o, m, n, k, EPI_BIAS, bias=bias, bn=1024)
+    _close(o, a.float() @ b.float().T + bias.float(), True)
+    o3 = torch.zeros(m, n, device="cuda", dtype=torch.float32)
+    _run(a, b, o3, m, n, k, EPI_F32, bn=1024)
+    _close(o3, a.float() @ b.float().T, False)

@@ -15,12 +15,16 @@ SHAPES = {  # name: (M, N, K, epilogue)
     "qkv_d64": (64, 6144, 4096, 0), "o_d64": (64, 4096, 4096, 2), "gate_up_d64": (64, 28672, 4096, 3),
     "down_d64": (64, 4096, 14336, 2), "gate_up_1100": (1100, 28672, 4096, 3),
 }
-VARIANTS = [(0, 0), (256, 1), (256, 3), (256, 5), (128, 3), (512, 0), (512, 1), (512, 3)]
+VARIANTS = [(0, 0), (256, 1), (256, 3), (256, 5), (512, 0), (1024, 0), (1024, 1), (1024, 2), (1024, 3), (1024, 5)]
 
 
 def main():
+    import os
     out = {}
+    only = [x for x in os.environ.get("GEMM_SHAPES", "").split(",") if x]
     for name, (m, n, k, epi) in SHAPES.items():
+        if only and name not in only:
+            continue
         a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
         b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.02
         o = torch.zeros(m, n // 2 if epi == 3 else n, device="cuda",
@@ -62,7 +66,7 @@ def main():
         out[name] = {"M": m, "N": n, "K": k, "us": res, "best_tflops": flops / best / 1e6 if best else None}
         print(name, {k: (round(v, 1) if isinstance(v, float) else v) for k, v in res.items()},
               "best TF/s %.0f" % (flops / best / 1e6), flush=True)
-    json.dump(out, open("gpurun_out/gemm_bench.json", "w"), indent=1)
+    json.dump(out, open(os.environ.get("GEMM_BENCH_OUT", "gpurun_out/gemm_bench.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
