@@ -398,6 +398,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;  // S0 @0, S1 @128, O0 @256, O1 @384
+  pdl_wait();  // q / K / V written by the QKV GEMM (the step metadata above came from a memcpy)
+  pdl_trigger();
 
   if (warp == 8 || warp == 9) {
     // ------------------------------------------------------------ TMA producers: warp 8 streams
@@ -718,6 +720,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_const
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // q / K / V written by the QKV GEMM (dec_cta_off above came from a memcpy)
+  pdl_trigger();
   const int qkv_ld = (p.n_heads + 2 * p.n_kv_heads) * DH;
 
   if (warp == kDecConsumers) {

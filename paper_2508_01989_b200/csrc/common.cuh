@@ -282,6 +282,15 @@ TC_DEVICE void bulk_wait_group() {
 // generic-proxy shared-memory writes -> visible to the async proxy (TMA) after a barrier
 TC_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Step kernels are launched with programmatic stream serialization: a kernel may start (barrier
+// init, TMEM alloc, descriptor prefetch) while its predecessor drains. pdl_wait() blocks until
+// the predecessor grid has completed and its memory is visible; every step kernel calls it
+// before its first global-memory access. pdl_trigger() lets the successor launch early.
+// Both are no-ops when the kernel was launched without the attribute.
+TC_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+TC_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- misc
 TC_DEVICE void st_global_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");

@@ -47,6 +47,8 @@ __global__ void init_weights(__nv_bfloat16* dst, long long rows, long long cols,
 // resid[t, :] = float(embed[tokens[t], :])
 __global__ void embed_rows(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed,
                            float* __restrict__ resid, int d) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const __nv_bfloat16* src = embed + (long long)tokens[t] * d;
   float* dst = resid + (long long)t * d;
@@ -74,6 +76,8 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict_
                                                         __nv_bfloat16* __restrict__ out, int d, float eps,
                                                         float* __restrict__ zero = nullptr, int zero_cols = 0) {
   constexpr int kMaxVec = 8192 / (4 * THREADS);
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
   const float* xr = x + (long long)src * d;
@@ -118,6 +122,8 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict_
 // ids[r] = argmax_v logits[r, v], lowest index on ties.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) argmax_rows(const float* __restrict__ logits, int vocab, int* __restrict__ ids) {
+  pdl_wait();
+  pdl_trigger();
   const float* row = logits + (long long)blockIdx.x * vocab;
   float best = -INFINITY;
   int best_i = 0x7fffffff;

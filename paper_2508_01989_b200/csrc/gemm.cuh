@@ -295,6 +295,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // predecessor kernel's outputs (activations, residual) are visible from here on
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -516,6 +518,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // ---------------------------------------------------------------- streaming-mode finishers
 // SwiGLU over the fp32 scratch of a 64-interleaved gate|up GEMM: act[m, j] = silu(g) * u.
 __global__ void finish_swiglu(const float* __restrict__ scr, int M, int F, __nv_bfloat16* __restrict__ act) {
+  pdl_wait();
+  pdl_trigger();
   const long long n4 = (long long)M * F / 4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 4;
@@ -535,6 +539,8 @@ __global__ void finish_swiglu(const float* __restrict__ scr, int M, int F, __nv_
 // (row, head, rotation pair j < head_dim / 2).
 __global__ void finish_qkv_rope(const float* __restrict__ scr, int M, QkvRopeArgs r, const __nv_bfloat16* bias,
                                 __nv_bfloat16* __restrict__ q_out, int q_ld) {
+  pdl_wait();
+  pdl_trigger();
   const int half = r.head_dim / 2;
   const int heads = r.n_heads + 2 * r.n_kv_heads;
   const int N = heads * r.head_dim;
@@ -628,6 +634,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();  // barriers of both CTAs initialised before any cross-CTA arrive / TMA credit
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // predecessor kernel's outputs (activations, residual) are visible from here on
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {

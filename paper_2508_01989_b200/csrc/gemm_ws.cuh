@@ -207,6 +207,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // predecessor kernel's outputs (activations, residual) are visible from here on
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -286,6 +288,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           pos_pf[c] = ok ? __ldg(args.rope.positions + tok) : 0;
           kv_pf[c] = ok ? __ldg(args.rope.row_kv + tok) : 0;
         }
+        // pull this thread's (cos, sin) lines into L2: the table is evicted by the weight stream
+        // between layers, and a DRAM round trip per chunk would serialise the epilogue
+        const int half = args.rope.head_dim >> 1, j0 = (s * 16) % half;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c * 32 < TN && w.mt * TN + c * 32 + t < args.M)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.rope.rope_cs + (size_t)pos_pf[c] * half + j0));
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();

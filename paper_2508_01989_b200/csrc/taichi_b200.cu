@@ -130,6 +130,31 @@ CUtensorMap encode_map(void* base, int rank, const cuuint64_t* dims, const cuuin
   return m;
 }
 
+// Step kernels launch with programmatic stream serialization (PDL): each kernel's prologue
+// overlaps its predecessor's tail; the kernels order their memory accesses with
+// griddepcontrol.wait (common.cuh pdl_wait). TC_PDL=0 disables it (A/B switch).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TC_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 // ------------------------------------------------------------------ GEMM dispatch
 int device_sms(int dev) {
   static std::mutex mu;
@@ -264,12 +289,12 @@ void launch_gemm_bn(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Gemm
                     cudaStream_t s) {
   const int smem = tc::GemmCfg<BN>::kSmemBytes;
   switch (epi) {
-    case tc::EPI_BF16: tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_BF16_BIAS: tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_RESID_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_SWIGLU: tc::gemm_bf16_tcgen05<BN, tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_F32: tc::gemm_bf16_tcgen05<BN, tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
-    case tc::EPI_QKV_ROPE: tc::gemm_bf16_tcgen05<BN, tc::EPI_QKV_ROPE><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb, args); break;
+    case tc::EPI_BF16: launch_k(tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16>, grid, tc::kGemmThreads, smem, s, ma, mb, args); break;
+    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_bf16_tcgen05<BN, tc::EPI_BF16_BIAS>, grid, tc::kGemmThreads, smem, s, ma, mb, args); break;
+    case tc::EPI_RESID_F32: launch_k(tc::gemm_bf16_tcgen05<BN, tc::EPI_RESID_F32>, grid, tc::kGemmThreads, smem, s, ma, mb, args); break;
+    case tc::EPI_SWIGLU: launch_k(tc::gemm_bf16_tcgen05<BN, tc::EPI_SWIGLU>, grid, tc::kGemmThreads, smem, s, ma, mb, args); break;
+    case tc::EPI_F32: launch_k(tc::gemm_bf16_tcgen05<BN, tc::EPI_F32>, grid, tc::kGemmThreads, smem, s, ma, mb, args); break;
+    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_bf16_tcgen05<BN, tc::EPI_QKV_ROPE>, grid, tc::kGemmThreads, smem, s, ma, mb, args); break;
     default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
@@ -324,12 +349,12 @@ void launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb128, const tc::
                      cudaStream_t s) {
   const int smem = tc::Gemm2Cfg::kSmemBytes;
   switch (epi) {
-    case tc::EPI_BF16: tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
-    case tc::EPI_BF16_BIAS: tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
-    case tc::EPI_RESID_F32: tc::gemm_bf16_tcgen05_2sm<tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
-    case tc::EPI_SWIGLU: tc::gemm_bf16_tcgen05_2sm<tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
-    case tc::EPI_F32: tc::gemm_bf16_tcgen05_2sm<tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
-    case tc::EPI_QKV_ROPE: tc::gemm_bf16_tcgen05_2sm<tc::EPI_QKV_ROPE><<<grid, tc::kGemmThreads, smem, s>>>(ma, mb128, args); break;
+    case tc::EPI_BF16: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
+    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16_BIAS>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
+    case tc::EPI_RESID_F32: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_RESID_F32>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
+    case tc::EPI_SWIGLU: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_SWIGLU>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
+    case tc::EPI_F32: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_F32>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
+    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_QKV_ROPE>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
     default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
@@ -350,12 +375,12 @@ void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensor
                     int epi, int grid, cudaStream_t s) {
   const int smem = tc::kWsSmemBytes;
   switch (epi) {
-    case tc::EPI_BF16: tc::gemm_ws_2sm<tc::EPI_BF16><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
-    case tc::EPI_BF16_BIAS: tc::gemm_ws_2sm<tc::EPI_BF16_BIAS><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
-    case tc::EPI_RESID_F32: tc::gemm_ws_2sm<tc::EPI_RESID_F32><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
-    case tc::EPI_SWIGLU: tc::gemm_ws_2sm<tc::EPI_SWIGLU><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
-    case tc::EPI_F32: tc::gemm_ws_2sm<tc::EPI_F32><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
-    case tc::EPI_QKV_ROPE: tc::gemm_ws_2sm<tc::EPI_QKV_ROPE><<<grid, tc::kGemmThreads, smem, s>>>(mw, mx, mo, args); break;
+    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
     default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
@@ -574,6 +599,11 @@ struct tc_instance {
   int32_t* meta_dev = nullptr;
   size_t meta_ints = 0;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  // concurrent attention: prefill attention runs on stream_pf beside decode attention, on the
+  // SMs the (narrowed) decode grid leaves free
+  cudaStream_t stream_pf = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int pf_sms = 0;  // SMs left to prefill attention in this step (0 = serial)
   bool step_pending = false;
   int last_sampled = 0;
   int launches = 0;       // kernels launched by the last step
@@ -749,6 +779,8 @@ void alloc_buffers(tc_instance* I) {
   TC_CUDA(cudaMallocHost(&I->meta_host, I->meta_ints * 4));
   TC_CUDA(cudaMalloc(&I->meta_dev, I->meta_ints * 4));
   TC_CUDA(cudaEventCreate(&I->ev_start));
+  TC_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
+  TC_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
   TC_CUDA(cudaEventCreate(&I->ev_stop));
   TC_CUDA(cudaEventCreate(&I->mig_a));
   TC_CUDA(cudaEventCreate(&I->mig_b));
@@ -800,17 +832,31 @@ struct ProfScope {
 template <int DH, int G>
 void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int hk = I->d.n_kv_heads;
+  if (n_qblk > 0 && n_dec > 0 && I->pf_sms > 0) {
+    // decode on the main stream over sms - pf_sms CTAs (launched first, so its persistent CTAs
+    // take their SMs), prefill beside it on stream_pf over whatever SMs remain; join before O
+    TC_CUDA(cudaEventRecord(I->ev_fork, I->stream));
+    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    TC_CUDA(cudaStreamWaitEvent(I->stream_pf, I->ev_fork, 0));
+    launch_k(tc::attn_prefill_tc<DH, G>, dim3(n_qblk, hk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
+             I->kv2_map, I->q_map, p);
+    TC_CUDA(cudaEventRecord(I->ev_join, I->stream_pf));
+    TC_CUDA(cudaStreamWaitEvent(I->stream, I->ev_join, 0));
+    I->launches += 2;
+    TC_CUDA(cudaGetLastError());
+    return;
+  }
   if (n_qblk > 0) {
 #if TC_PREFILL_MMA_SYNC
     tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kPrefillThreads, tc::PrefillSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
 #else
-    tc::attn_prefill_tc<DH, G><<<dim3(n_qblk, hk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream>>>(I->kv2_map,
-                                                                                                       I->q_map, p);
+    launch_k(tc::attn_prefill_tc<DH, G>, dim3(n_qblk, hk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream,
+             I->kv2_map, I->q_map, p);
 #endif
     ++I->launches;
   }
   if (n_dec > 0) {
-    tc::attn_decode<DH, G><<<dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream>>>(I->kv_map, p);
+    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
     ++I->launches;
   }
   TC_CUDA(cudaGetLastError());
@@ -865,7 +911,30 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   const int n_seg = n_dec * m.n_kv_heads;
   long long W = 0;
   for (int i = 0; i < n_dec; ++i) W += (long long)(st->decode[i].pos / ps + 1) * m.n_kv_heads;
-  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(I->sms, (W + 7) / 8)) : 0;
+  // Mixed steps run prefill attention beside decode attention (pf_sms SMs left to prefill).
+  // Balance: prefill CTA-time ~ 2.5 us per 128-key tile per CTA (B200, Llama-3-8B shapes; the
+  // measured optimum at P=512 over a 512 prefix + 64 decodes @1k is 40 SMs) over
+  // pf_sms SMs vs decode at ~5.2 TB/s over the rest. TC_PF_SMS overrides (0 = serial).
+  I->pf_sms = 0;
+  if (n_dec > 0 && n_qblk > 0) {
+    long long pf_tiles = 0;
+    for (int i = 0; i < n_pf; ++i) {
+      const tc_prefill_slice& sl = st->prefill[i];
+      for (int q = 0; q < sl.n_tokens; q += tpc) pf_tiles += (sl.pos0 + std::min(q + tpc, sl.n_tokens) + 127) / 128;
+    }
+    pf_tiles *= m.n_kv_heads;
+    const double pf_cta_us = 2.5 * (double)pf_tiles * (m.head_dim / 128.0);
+    const double dec_us = (double)W * ps * m.head_dim * 2 * 2 / 5.2e6;  // K + V bytes / (5.2 TB/s)
+    int want = (int)std::ceil(pf_cta_us / std::max(dec_us, 1.0));
+    static const int env_pf = [] {
+      const char* e = std::getenv("TC_PF_SMS");
+      return e ? std::atoi(e) : -1;
+    }();
+    if (env_pf >= 0) want = env_pf;
+    I->pf_sms = std::max(0, std::min({want, n_qblk * m.n_kv_heads, I->sms / 2}));
+  }
+  const int dec_sms = I->sms - I->pf_sms;
+  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_sms, (W + 7) / 8)) : 0;
   // entries: one per (CTA, segment overlap); at most n_seg + dec_grid
   const int max_entries = n_seg + dec_grid;
   // layout of the metadata block
@@ -986,7 +1055,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
 
   {
     ProfScope ps_(I, "embed");
-    tc::embed_rows<<<T, 256, 0, s>>>(dm + o_tok, I->embed, I->resid, m.d_model);
+    launch_k(tc::embed_rows, T, 256, 0, s, dm + o_tok, I->embed, I->resid, m.d_model);
     ++I->launches;
   }
   tc::AttnParams ap{};
@@ -1033,7 +1102,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     const LayerW& L = I->layers[l];
     {
       ProfScope p_(I, "norm");
-      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps,
+      launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps,
                                                               streaming ? I->stream_scr : nullptr, I->qkv_n);
       ++I->launches;
     }
@@ -1044,7 +1113,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.qkv, T, nullptr, I->qkv_n, nullptr, tc::EPI_BF16, I->sms, I->sk, s, 0, 0,
                                 nullptr, I->stream_scr);
-        tc::finish_qkv_rope<<<fin_blocks, 256, 0, s>>>(I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
+        launch_k(tc::finish_qkv_rope, fin_blocks, 256, 0, s, I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
                                                       I->qkv_n);
         ++I->launches;
       } else {
@@ -1064,7 +1133,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "norm");
-      tc::rmsnorm_rows<rms_threads><<<T, rms_threads, 0, s>>>(I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps,
+      launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps,
                                                               streaming ? I->stream_scr : nullptr, 2 * m.ffn_dim);
       ++I->launches;
     }
@@ -1073,7 +1142,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, nullptr, m.ffn_dim, nullptr, tc::EPI_BF16, I->sms, I->sk, s,
                                 0, 0, nullptr, I->stream_scr);
-        tc::finish_swiglu<<<fin_blocks, 256, 0, s>>>(I->stream_scr, T, m.ffn_dim, I->act);
+        launch_k(tc::finish_swiglu, fin_blocks, 256, 0, s, I->stream_scr, T, m.ffn_dim, I->act);
         ++I->launches;
       } else {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
@@ -1087,11 +1156,11 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   }
   if (n_logit > 0) {
     ProfScope p_(I, "lm_head");
-    tc::rmsnorm_rows<rms_threads><<<n_logit, rms_threads, 0, s>>>(I->resid, dm + o_lrow, I->final_norm, I->lm_in,
-                                                                  m.d_model, m.rms_eps);
+    launch_k(tc::rmsnorm_rows<rms_threads>, n_logit, rms_threads, 0, s, I->resid, dm + o_lrow, I->final_norm, I->lm_in,
+             m.d_model, m.rms_eps, (float*)nullptr, 0);
     I->launches += 2;  // gathered RMSNorm + argmax
     I->launches += run_gemm(I->map_lm_in, I->lm_head, n_logit, I->logits, m.vocab, nullptr, tc::EPI_F32, I->sms, I->sk, s);
-    tc::argmax_rows<1024><<<n_logit, 1024, 0, s>>>(I->logits, m.vocab, I->ids_dev);
+    launch_k(tc::argmax_rows<1024>, n_logit, 1024, 0, s, I->logits, m.vocab, I->ids_dev);
     TC_CUDA(cudaMemcpyAsync(I->ids_host, I->ids_dev, (size_t)n_logit * 4, cudaMemcpyDeviceToHost, s));
   }
   TC_CUDA(cudaGetLastError());
@@ -1131,10 +1200,11 @@ void destroy(tc_instance* I) {
   if (I->ids_host) cudaFreeHost(I->ids_host);
   if (I->meta_host) cudaFreeHost(I->meta_host);
   if (I->mig_host) cudaFreeHost(I->mig_host);
-  for (cudaEvent_t e : {I->ev_start, I->ev_stop, I->mig_a, I->mig_b})
+  for (cudaEvent_t e : {I->ev_start, I->ev_stop, I->mig_a, I->mig_b, I->ev_fork, I->ev_join})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : I->prof.pool) cudaEventDestroy(e);
   if (I->stream) cudaStreamDestroy(I->stream);
+  if (I->stream_pf) cudaStreamDestroy(I->stream_pf);
   delete I;
 }
 
@@ -1243,6 +1313,7 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     I->sms = device_sms(desc->device);
     init_kernel_attrs(desc->device);
     TC_CUDA(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+    TC_CUDA(cudaStreamCreateWithFlags(&I->stream_pf, cudaStreamNonBlocking));
     if (desc->share_weights) {
       const tc_instance* o = desc->share_weights;
       TC_REQUIRE(o->desc.device == desc->device, "create: share_weights needs the same device");
