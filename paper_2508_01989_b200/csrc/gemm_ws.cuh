@@ -207,21 +207,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // predecessor kernel's outputs (activations, residual) are visible from here on
+  // predecessor kernel's outputs (activations, residual) are visible after pdl_wait; the TMA
+  // producer waits later, after it has issued the weight loads of its first stages
+  if (!(warp == 0 && lane == 0)) pdl_wait();
   pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
       const int half_tn = TN / 2;
-      int stage = 0;
+      const int wrow = (int)rank * 128;
+      // Weights do not depend on the predecessor kernel: fill the first ring stages with this
+      // CTA's weight k-blocks while the predecessor drains (PDL), then wait for the activations.
+      int pre = 0;
+      if (pair < args.units) {
+        const Unit w0 = unit_of(args, pair);
+        pre = min(S, w0.k1 - w0.k0);
+        for (int i = 0; i < pre; ++i) {
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[i], 2 * stage_bytes);
+          tma_load_2d_2sm(smem + i * stage_bytes, &map_w, &full_bar[i], (w0.k0 + i) * kGemmBK, w0.nt * 256 + wrow,
+                          kEvictNormal);
+        }
+      }
+      pdl_wait();
+      int stage = 0, issued = 0;
       uint32_t phase = 0;
       for (int u = pair; u < args.units; u += n_pairs) {
         const Unit w = unit_of(args, u);  // w.mt = token tile, w.nt = weight pair tile
-        for (int kb = w.k0; kb < w.k1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_bytes);
+        for (int kb = w.k0; kb < w.k1; ++kb, ++issued) {
           uint8_t* st = smem + stage * stage_bytes;
-          tma_load_2d_2sm(st, &map_w, &full_bar[stage], kb * kGemmBK, w.nt * 256 + (int)rank * 128, kEvictNormal);
+          if (issued >= pre) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_bytes);
+            tma_load_2d_2sm(st, &map_w, &full_bar[stage], kb * kGemmBK, w.nt * 256 + wrow, kEvictNormal);
+          }
+#if TC_WS_L2_PREFETCH
+          // keep the DRAM weight stream a ring's depth further ahead through L2 (off: it wins in the
+          // isolated microbench but costs 3% in the step, where L2 also holds the activations)
+          if (kb + S < w.k1) tma_prefetch_2d_l2(&map_w, (kb + S) * kGemmBK, w.nt * 256 + wrow);
+#endif
           tma_load_2d_2sm(st + kWsWBytes, &map_x, &full_bar[stage], kb * kGemmBK, w.mt * TN + (int)rank * half_tn,
                           kEvictLast);
           if (++stage == S) {
