@@ -449,9 +449,18 @@ int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfl
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
   TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256 || force_bn == 512 || force_bn == 1024,
              "gemm: tile width must be 128, 256, 512 (= 2-SM 256 x 256) or 1024 (= weight-stationary pair)");
-  if (red_out == nullptr && N % 256 == 0 &&
-      (force_bn == 1024 || (force_bn == 0 && ws_enabled() && M > kWsMinRows && epi != tc::EPI_F32)))
+  static const bool ws_small = [] {
+    const char* e = std::getenv("TC_WS_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  if (N % 256 == 0 && epi != tc::EPI_F32 &&
+      (force_bn == 1024 || (force_bn == 0 && ws_enabled() && (M > kWsMinRows || ws_small)))) {
+    // streaming mode (decode-only steps): split-K partials land in the zeroed fp32 scratch via
+    // TMA bulk adds; the finish kernel applies RoPE + KV append / SwiGLU
+    if (red_out != nullptr) return run_gemm_ws(a, w, M, red_out, N, nullptr, tc::EPI_RESID_F32, sms, s, force_splits,
+                                               nullptr, nullptr);
     return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map);
+  }
   const CUtensorMap& a_map = a.m128;
   const bool two_sm = N % 256 == 0 && (force_bn == 512 || (force_bn == 0 && M > kGemm2MinM));
   if (two_sm) {
