@@ -83,6 +83,7 @@ struct GemmArgs {
                              // zeroed fp32 [M, N] scratch; a finish kernel applies the epilogue
   int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
   int stages;                // gemm_ws_2sm: smem ring depth for this token tile
+  unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][8]
 };
 
 template <int BN>

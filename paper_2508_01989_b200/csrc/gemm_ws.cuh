@@ -187,6 +187,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  // tools-only timeline: 0 entry, 1 prologue done, 2 first stage landed (MMA), 3 last MMA issued,
+  // 4 epilogue of the first unit done, 5 epilogue of the last unit done
+  auto stamp = [&](int i) {
+    if (args.trace) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      args.trace[blockIdx.x * 8 + i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   if (warp == 0 && lane == 0) {
@@ -207,6 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
   // predecessor kernel's outputs (activations, residual) are visible after pdl_wait; the TMA
   // producer waits later, after it has issued the weight loads of its first stages
   if (!(warp == 0 && lane == 0)) pdl_wait();
@@ -271,6 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int kb = w.k0; kb < w.k1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (local == 1 && kb == w.k0 && lane == 0) stamp(2);
           if (elect_one()) {
             const uint32_t w_addr = smem_u32(smem + stage * stage_bytes);
             const uint32_t x_addr = w_addr + kWsWBytes;
@@ -279,7 +291,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               umma_bf16_2sm(d_tmem, umma_smem_desc<kGemmBK * 2>(w_addr + k * 32),
                             umma_smem_desc<kGemmBK * 2>(x_addr + k * 32), idesc, (kb > w.k0 || k > 0) ? 1u : 0u);
             umma_commit_2sm_multicast(&empty_bar[stage]);
-            if (kb == w.k1 - 1) umma_commit_2sm_multicast(&tfull_bar[acc]);
+            if (kb == w.k1 - 1) {
+              umma_commit_2sm_multicast(&tfull_bar[acc]);
+              stamp(3);
+            }
           }
           __syncwarp();
           if (++stage == S) {
@@ -359,6 +374,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, pos_pf[ci], kv_pf[ci]);
         }
       }
+      if (et == 0) {
+        if (local == 1) stamp(4);
+        stamp(5);
+      }
     }
   }
 
@@ -368,6 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_2sm(tmem_base, 512);
+    if (lane == 0) stamp(6);
   }
 }
 

@@ -429,6 +429,14 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     args.rope = *rope;
   }
   const int grid = 2 * (int)std::min<long long>(pairs, args.units);
+  // TC_WS_TRACE=1 (tools only): per-CTA %globaltimer timeline of this launch printed to stderr
+  static const bool trace = std::getenv("TC_WS_TRACE") != nullptr;
+  unsigned long long* trace_dev = nullptr;
+  if (trace) {
+    TC_CUDA(cudaMalloc(&trace_dev, (size_t)grid * 8 * 8));
+    TC_CUDA(cudaMemsetAsync(trace_dev, 0, (size_t)grid * 8 * 8, s));
+    args.trace = trace_dev;
+  }
   CUtensorMap resid_map;
   if (epi == tc::EPI_RESID_F32) {
     // the residual's TMA map: the instance's (built once) or, for tc_gemm, one over `out`
@@ -437,6 +445,26 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   }
   launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), args, epi, grid, s);
   TC_CUDA(cudaGetLastError());
+  if (trace) {
+    std::vector<unsigned long long> h((size_t)grid * 8);
+    TC_CUDA(cudaMemcpyAsync(h.data(), trace_dev, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    cudaFree(trace_dev);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < grid; ++b)
+      if (h[b * 8]) t0 = std::min(t0, h[b * 8]);
+    std::fprintf(stderr, "ws_trace M=%d N=%d K=%d epi=%d tn=%d units=%d splits=%d grid=%d (us from first entry: min/med/max)\n",
+                 M, N, K, epi, args.tn, args.units, args.splits, grid);
+    const char* names[7] = {"entry", "prologue", "first_stage", "last_mma", "epi_first", "epi_last", "exit"};
+    for (int e = 0; e < 7; ++e) {
+      std::vector<double> v;
+      for (int b = 0; b < grid; ++b)
+        if (h[b * 8 + e]) v.push_back((h[b * 8 + e] - t0) / 1e3);
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      std::fprintf(stderr, "  %-12s %8.2f %8.2f %8.2f  (n=%zu)\n", names[e], v.front(), v[v.size() / 2], v.back(), v.size());
+    }
+  }
   return 1;
 }
 
