@@ -35,7 +35,11 @@ constexpr int kWsWBytes = 128 * kGemmBK * 2;           // this CTA's 128 weight 
 constexpr int kWsStagingFloats = 32 * 128;             // one 32-token x 128-feature fp32 chunk
 constexpr int kWsSmemBytes = 232448;                   // max dynamic shared memory per CTA (sm_100)
 constexpr int kWsBarBytes = 256;
-constexpr int kWsRingBudget = kWsSmemBytes - 1024 - 2 * kWsStagingFloats * 4 - kWsBarBytes;
+constexpr int kWsMetaBytes = 2 * 2 * 256 * 4;          // per-unit-parity token metadata (pos, kv row)
+constexpr int kWsRingBudget = kWsSmemBytes - 1024 - 2 * kWsStagingFloats * 4 - kWsMetaBytes - kWsBarBytes;
+// warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 epilogue group 0 (even 32-token chunks),
+// 8-11 epilogue group 1 (odd chunks): two groups hide each other's TMEM / smem / store latency
+constexpr int kWsThreads = 384;
 
 __host__ __device__ constexpr int ws_stage_bytes(int tn) { return kWsWBytes + (tn / 2) * kGemmBK * 2; }
 __host__ __device__ constexpr int ws_stages(int tn) {
@@ -171,15 +175,16 @@ __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const floa
 // (cp.reduce.async.bulk.tensor .add), which also reduces the split-K partials.
 // args.m_tiles = token tiles, args.n_tiles = 256-row weight pair tiles, args.tn, args.stages.
 template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
     gemm_ws_2sm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                 const __grid_constant__ CUtensorMap map_o, GemmArgs args) {
   const int TN = args.tn, S = args.stages;
   const int stage_bytes = ws_stage_bytes(TN);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* stg = reinterpret_cast<float*>(smem + S * stage_bytes);  // [2][32][128]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + 2 * kWsStagingFloats);
+  float* stg = reinterpret_cast<float*>(smem + S * stage_bytes);  // [group][32][128]
+  int* meta = reinterpret_cast<int*>(stg + 2 * kWsStagingFloats);  // [unit parity][pos | kv row][256]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta + 2 * 2 * 256);
   uint64_t* empty_bar = full_bar + kWsMaxStages;
   uint64_t* tfull_bar = empty_bar + kWsMaxStages;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;            // [2] (leader's copy is used)
@@ -208,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty_bar[a], 16);  // 8 epilogue warps x 2 CTAs
     }
     mbar_fence_init();
   }
@@ -305,83 +310,96 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;              // TMEM lane quarter
-    const int f = ew * 32 + lane;         // weight row within this CTA's 128 (transposed write)
-    const int et = threadIdx.x - 128;     // 0..127
-    const int t = et >> 2, s = et & 3;    // token row / 32-feature segment (row phase)
+    const int grp = (warp - 4) >> 2;            // epilogue group: chunks ci with ci % 2 == grp
+    const int ew = warp & 3;                    // TMEM lane quarter (warp % 4)
+    const int f = ew * 32 + lane;               // weight row within this CTA's 128 (transposed write)
+    const int et = (threadIdx.x - 128) & 127;   // thread within the group
+    const int t = et >> 2, s = et & 3;          // token row / 32-feature segment (row phase)
     const int fch = f >> 2, fe = f & 3;
-    int local = 0, chunk_ctr = 0;
+    const uint32_t gbar = 1 + grp;              // named barrier of this group (128 threads)
+    float* sb = stg + grp * kWsStagingFloats;
+    const int n_chunks = TN / 32;
+    int local = 0;
     for (int u = pair; u < args.units; u += n_pairs) {
       const Unit w = unit_of(args, u);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       ++local;
-      // per-token RoPE / KV-append metadata of this thread's rows, fetched while the MMAs run
-      int pos_pf[8], kv_pf[8];
+      int* mpos = meta + acc * 512;
+      int* mkv = mpos + 256;
       if constexpr (EPI == EPI_QKV_ROPE) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int tok = w.mt * TN + c * 32 + t;
-          const bool ok = c * 32 < TN && tok < args.M;
-          pos_pf[c] = ok ? __ldg(args.rope.positions + tok) : 0;
-          kv_pf[c] = ok ? __ldg(args.rope.row_kv + tok) : 0;
+        // this unit's per-token RoPE / KV-append metadata -> smem (both groups), fetched while
+        // the MMAs run; the rows' (cos, sin) lines are pulled into L2 (the weight stream evicts
+        // the table between layers)
+        const int e2 = threadIdx.x - 128;  // 0..255
+        const int tok = w.mt * TN + e2;
+        if (e2 < TN) {
+          const bool ok = tok < args.M;
+          const int pos = ok ? __ldg(args.rope.positions + tok) : 0;
+          mpos[e2] = pos;
+          mkv[e2] = ok ? __ldg(args.rope.row_kv + tok) : 0;
+          if (ok) {
+            const int half = args.rope.head_dim >> 1;
+            for (int c = 0; c < half; c += 32)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(args.rope.rope_cs + (size_t)pos * half + c));
+          }
         }
-        // pull this thread's (cos, sin) lines into L2: the table is evicted by the weight stream
-        // between layers, and a DRAM round trip per chunk would serialise the epilogue
-        const int half = args.rope.head_dim >> 1, j0 = (s * 16) % half;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c * 32 < TN && w.mt * TN + c * 32 + t < args.M)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.rope.rope_cs + (size_t)pos_pf[c] * half + j0));
+        asm volatile("bar.sync 3, 256;" ::: "memory");
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (et == 0 && grp == 0) stamp(7);
       const int fbase = w.nt * 256 + (int)rank * 128;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
-#pragma unroll
-      for (int ci = 0; ci < 8; ++ci) {
+      const int my_last = (n_chunks - 1 - grp) >= 0 ? ((n_chunks - 1 - grp) & ~1) + grp : -1;
+      if (my_last < 0) {  // a single-chunk tile leaves group 1 idle: release its share at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
+      }
+#pragma unroll 1
+      for (int ci = grp; ci < n_chunks; ci += 2) {
         const int c0 = ci * 32;
-        if (c0 >= TN) break;
-        ++chunk_ctr;
-        float* sb = stg + (chunk_ctr & 1) * kWsStagingFloats;
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c0, r);
         tmem_ld_wait();
-        if (c0 + 32 >= TN) {  // accumulator fully read: release it to the MMA warp early
+        if (ci == my_last) {  // this warp's last read of the accumulator: release it early
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
         }
         if constexpr (EPI == EPI_RESID_F32) {
           // dense [32 tokens][128 features] chunk -> one TMA bulk add into the residual; the
-          // issuing thread first makes sure the reduction that last read this buffer is done
-          if (et == 0) bulk_wait_group_read<1>();
-          epi_bar();
+          // group's issuing thread first makes sure its previous reduction finished reading sb
+          if (et == 0) bulk_wait_group_read<0>();
+          asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
           const int tok0 = w.mt * TN + c0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) sb[i * 128 + f] = tok0 + i < args.M ? __uint_as_float(r[i]) : 0.f;
           fence_async_smem();
-          epi_bar();
+          asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
           if (et == 0) {
             tma_reduce_add_2d(&map_o, smem_u32(sb), fbase, tok0);
             bulk_commit_group();
           }
         } else {
+          asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");  // previous row phase done with sb
 #pragma unroll
           for (int i = 0; i < 32; ++i) sb[ws_stg_idx(i, fch) + fe] = __uint_as_float(r[i]);
-          epi_bar();
+          asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
           const int tok = w.mt * TN + c0 + t;
-          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, pos_pf[ci], kv_pf[ci]);
+          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
         }
       }
-      if (et == 0) {
+      if (et == 0 && grp == 0) {
         if (local == 1) stamp(4);
         stamp(5);
       }
     }
   }
 
-  if (EPI == EPI_RESID_F32 && threadIdx.x == 128) bulk_wait_group<0>();  // residual updates landed
+  // the staged residual chunks must have been read by the TMA unit before the CTA's smem goes away
+  if (EPI == EPI_RESID_F32 && warp >= 4 && ((threadIdx.x - 128) & 127) == 0) bulk_wait_group_read<0>();
   tc_fence_before();
   cluster_sync();  // every MMA retired and both epilogues drained before TMEM is released
   if (warp == 2) {

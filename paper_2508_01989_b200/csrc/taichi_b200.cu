@@ -375,12 +375,12 @@ void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensor
                     int epi, int grid, cudaStream_t s) {
   const int smem = tc::kWsSmemBytes;
   switch (epi) {
-    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kGemmThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
     default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
@@ -455,8 +455,9 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
       if (h[b * 8]) t0 = std::min(t0, h[b * 8]);
     std::fprintf(stderr, "ws_trace M=%d N=%d K=%d epi=%d tn=%d units=%d splits=%d grid=%d (us from first entry: min/med/max)\n",
                  M, N, K, epi, args.tn, args.units, args.splits, grid);
-    const char* names[7] = {"entry", "prologue", "first_stage", "last_mma", "epi_first", "epi_last", "exit"};
-    for (int e = 0; e < 7; ++e) {
+    const char* names[8] = {"entry", "prologue", "first_stage", "last_mma", "epi_first", "epi_last", "exit",
+                            "epi_start_last"};
+    for (int e = 0; e < 8; ++e) {
       std::vector<double> v;
       for (int b = 0; b < grid; ++b)
         if (h[b * 8 + e]) v.push_back((h[b * 8 + e] - t0) / 1e3);
@@ -481,8 +482,8 @@ int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfl
     const char* e = std::getenv("TC_WS_SMALL");
     return !(e && e[0] == '0');
   }();
-  if (N % 256 == 0 && epi != tc::EPI_F32 &&
-      (force_bn == 1024 || (force_bn == 0 && ws_enabled() && (M > kWsMinRows || ws_small)))) {
+  if (N % 256 == 0 &&
+      (force_bn == 1024 || (force_bn == 0 && ws_enabled() && epi != tc::EPI_F32 && (M > kWsMinRows || ws_small)))) {
     // streaming mode (decode-only steps): split-K partials land in the zeroed fp32 scratch via
     // TMA bulk adds; the finish kernel applies RoPE + KV append / SwiGLU
     if (red_out != nullptr) return run_gemm_ws(a, w, M, red_out, N, nullptr, tc::EPI_RESID_F32, sms, s, force_splits,
