@@ -84,6 +84,8 @@ struct GemmArgs {
   int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
   int stages;                // gemm_ws_2sm: smem ring depth for this token tile
   unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][8]
+  int streamk;               // gemm_ws_2sm, residual epilogue: pair p takes k-blocks
+                             // [W p / P, W (p+1) / P) of the tile-major stream (W = tiles * kb)
 };
 
 template <int BN>
@@ -518,17 +520,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // ---------------------------------------------------------------- streaming-mode finishers
 // SwiGLU over the fp32 scratch of a 64-interleaved gate|up GEMM: act[m, j] = silu(g) * u.
-__global__ void finish_swiglu(const float* __restrict__ scr, int M, int F, __nv_bfloat16* __restrict__ act) {
+// Each finisher zeroes the scratch it consumed, so the next streaming GEMM can accumulate into it
+// without a separate clearing pass (the scratch is zeroed once at instance creation).
+__global__ void finish_swiglu(float* __restrict__ scr, int M, int F, __nv_bfloat16* __restrict__ act) {
   pdl_wait();
   pdl_trigger();
   const long long n4 = (long long)M * F / 4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 4;
     const int m = (int)(e / F), j = (int)(e % F);
-    const float* row = scr + (size_t)m * 2 * F;
+    float* row = scr + (size_t)m * 2 * F;
     const int gc = (j / 64) * 128 + (j % 64);
     const float4 g = *reinterpret_cast<const float4*>(row + gc);
     const float4 u = *reinterpret_cast<const float4*>(row + gc + 64);
+    *reinterpret_cast<float4*>(row + gc) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(row + gc + 64) = make_float4(0.f, 0.f, 0.f, 0.f);
     uint2 w;
     w.x = pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y);
     w.y = pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w);
@@ -538,7 +544,7 @@ __global__ void finish_swiglu(const float* __restrict__ scr, int M, int F, __nv_
 
 // (+bias) -> RoPE(q, k) -> q into q_out, k / v into the paged pool; one thread per
 // (row, head, rotation pair j < head_dim / 2).
-__global__ void finish_qkv_rope(const float* __restrict__ scr, int M, QkvRopeArgs r, const __nv_bfloat16* bias,
+__global__ void finish_qkv_rope(float* __restrict__ scr, int M, QkvRopeArgs r, const __nv_bfloat16* bias,
                                 __nv_bfloat16* __restrict__ q_out, int q_ld) {
   pdl_wait();
   pdl_trigger();
@@ -552,6 +558,8 @@ __global__ void finish_qkv_rope(const float* __restrict__ scr, int M, QkvRopeArg
     const int m = (int)(i / ((long long)half * heads));
     const int c = head * r.head_dim + j;
     float lo = scr[(size_t)m * N + c], hi = scr[(size_t)m * N + c + half];
+    scr[(size_t)m * N + c] = 0.f;
+    scr[(size_t)m * N + c + half] = 0.f;
     if (bias) {
       lo += __bfloat162float(bias[c]);
       hi += __bfloat162float(bias[c + half]);

@@ -169,6 +169,41 @@ __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const floa
   }
 }
 
+// Work iterator shared by the producer, MMA and epilogue roles of one pair (identical sequences).
+// Default: units u = pair, pair + n_pairs, ... (tile, k-split). Stream-K (residual epilogue, where
+// every partial is a TMA bulk add): the pair's contiguous range of the tile-major k-block stream,
+// cut at tile boundaries -- equal k-blocks per pair whatever the tile count (decode-only steps:
+// 112 gate_up tiles on 74 pairs would otherwise leave half the pairs a second full tile).
+struct WsIter {
+  long long pos, end;  // stream-K
+  int u;               // units
+};
+__device__ __forceinline__ WsIter ws_iter_begin(const GemmArgs& a, int pair, int n_pairs) {
+  WsIter it;
+  it.u = pair;
+  const long long total = (long long)a.m_tiles * a.n_tiles * a.kb;
+  it.pos = total * pair / n_pairs;
+  it.end = total * (pair + 1) / n_pairs;
+  return it;
+}
+__device__ __forceinline__ bool ws_next(const GemmArgs& a, WsIter& it, int n_pairs, Unit& w) {
+  if (!a.streamk) {
+    if (it.u >= a.units) return false;
+    w = unit_of(a, it.u);
+    it.u += n_pairs;
+    return true;
+  }
+  if (it.pos >= it.end) return false;
+  const int tile = (int)(it.pos / a.kb);
+  w.k0 = (int)(it.pos - (long long)tile * a.kb);
+  w.k1 = (int)min((long long)a.kb, w.k0 + (it.end - it.pos));
+  w.mt = tile % a.m_tiles;
+  w.nt = tile / a.m_tiles;
+  w.ks = 0;
+  it.pos += w.k1 - w.k0;
+  return true;
+}
+
 // map_w: weights [N, K], box 64 x 128 rows; map_x: activations [rows, K], box 64 x TN/2 rows;
 // map_o (EPI_RESID_F32 only): the fp32 residual [rows, N], box 128 features x 32 tokens, no
 // swizzle -- each 32-token chunk is staged densely and added by one TMA bulk reduction
@@ -235,8 +270,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
       // Weights do not depend on the predecessor kernel: fill the first ring stages with this
       // CTA's weight k-blocks while the predecessor drains (PDL), then wait for the activations.
       int pre = 0;
-      if (pair < args.units) {
-        const Unit w0 = unit_of(args, pair);
+      WsIter it = ws_iter_begin(args, pair, n_pairs);
+      Unit w0;
+      if (ws_next(args, it, n_pairs, w0)) {
         pre = min(S, w0.k1 - w0.k0);
         for (int i = 0; i < pre; ++i) {
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[i], 2 * stage_bytes);
@@ -247,8 +283,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
       pdl_wait();
       int stage = 0, issued = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < args.units; u += n_pairs) {
-        const Unit w = unit_of(args, u);  // w.mt = token tile, w.nt = weight pair tile
+      it = ws_iter_begin(args, pair, n_pairs);
+      Unit w;  // w.mt = token tile, w.nt = weight pair tile
+      while (ws_next(args, it, n_pairs, w)) {
         for (int kb = w.k0; kb < w.k1; ++kb, ++issued) {
           uint8_t* st = smem + stage * stage_bytes;
           if (issued >= pre) {
@@ -276,8 +313,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int u = pair; u < args.units; u += n_pairs) {
-        const Unit w = unit_of(args, u);
+      WsIter it = ws_iter_begin(args, pair, n_pairs);
+      Unit w;
+      while (ws_next(args, it, n_pairs, w)) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         ++local;
@@ -320,8 +358,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
     float* sb = stg + grp * kWsStagingFloats;
     const int n_chunks = TN / 32;
     int local = 0;
-    for (int u = pair; u < args.units; u += n_pairs) {
-      const Unit w = unit_of(args, u);
+    WsIter it = ws_iter_begin(args, pair, n_pairs);
+    Unit w;
+    while (ws_next(args, it, n_pairs, w)) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       ++local;

@@ -420,6 +420,21 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   }
   args.splits = std::max(1, std::min(sp, args.kb));
   args.units = (int)(tiles * args.splits);
+  // residual epilogue (incl. the decode-only streaming scratch) with one token tile and more weight
+  // tiles than pairs (decode-only gate_up: 112 on 74): stream-K evens the k-blocks per pair
+  // (-5%). With several token tiles the tile-major stream would separate the sibling pairs that
+  // share a weight tile (its L2 reuse; down +15%), and with fewer tiles than pairs the k-split
+  // units already fill one wave. TC_WS_STREAMK=0 disables it, =2 forces it (A/B).
+  static const int streamk_mode = [] {
+    const char* e = std::getenv("TC_WS_STREAMK");
+    return e ? std::atoi(e) : 1;
+  }();
+  args.streamk = (epi == tc::EPI_RESID_F32 && force_splits == 0 &&
+                  (streamk_mode == 2 || (streamk_mode == 1 && n_tt == 1 && tiles > pairs))) ? 1 : 0;
+  if (args.streamk) {
+    args.splits = 1;
+    args.units = (int)std::min<long long>(pairs, tiles * args.kb);  // one k-block range per pair
+  }
   args.out = out;
   args.ldo = ldo;
   args.bias = bias;
@@ -788,6 +803,8 @@ void alloc_buffers(tc_instance* I) {
     I->q_map = encode_map(I->qkv, 3, dims, strides, box);
   }
   TC_CUDA(cudaMalloc(&I->stream_scr, (size_t)kStreamRows * std::max<int64_t>(I->qkv_n, 2 * (int64_t)m.ffn_dim) * 4));
+  // zero once; the finish kernels re-zero what they consume (no per-step clearing pass)
+  TC_CUDA(cudaMemset(I->stream_scr, 0, (size_t)kStreamRows * std::max<int64_t>(I->qkv_n, 2 * (int64_t)m.ffn_dim) * 4));
   // stream-K partial slots + tile counters (counters must start at zero)
   TC_CUDA(cudaMalloc(&I->sk.ws, kSkWsBytes));
   TC_CUDA(cudaMalloc(&I->sk.cnt, (size_t)kSkMaxTiles * 4));
@@ -1141,7 +1158,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     {
       ProfScope p_(I, "norm");
       launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps,
-                                                              streaming ? I->stream_scr : nullptr, I->qkv_n);
+                                                              (float*)nullptr, 0);
       ++I->launches;
     }
     {
@@ -1172,7 +1189,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     {
       ProfScope p_(I, "norm");
       launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps,
-                                                              streaming ? I->stream_scr : nullptr, 2 * m.ffn_dim);
+                                                              (float*)nullptr, 0);
       ++I->launches;
     }
     {

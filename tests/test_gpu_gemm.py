@@ -141,8 +141,11 @@ def test_gemm_ws_bf16(cuda_ok, m, n, k):
     _close(out, a.float() @ b.float().T, True)
 
 
+# (64, 28672, ...) and (200, 20480, ...): one token tile, more weight tiles than CTA pairs -> the
+# stream-K partition (each pair a contiguous k-block range across tile boundaries)
 @pytest.mark.parametrize("m,n,k,splits", [(576, 4096, 14336, 0), (576, 4096, 4096, 3), (576, 4096, 4096, 1),
-                                          (64, 4096, 4096, 0), (333, 5120, 13824, 0), (7, 256, 512, 2)])
+                                          (64, 4096, 4096, 0), (333, 5120, 13824, 0), (7, 256, 512, 2),
+                                          (64, 28672, 1024, 0), (200, 20480, 704, 0)])
 def test_gemm_ws_residual(cuda_ok, m, n, k, splits):
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.02
