@@ -548,42 +548,65 @@ __global__ void finish_qkv_rope(float* __restrict__ scr, int M, QkvRopeArgs r, c
                                 __nv_bfloat16* __restrict__ q_out, int q_ld) {
   pdl_wait();
   pdl_trigger();
-  const int half = r.head_dim / 2;
+  // one thread per (row, head, 8 consecutive rotation pairs): 16 B vector loads / stores
+  const int half = r.head_dim / 2, groups = half / 8;
   const int heads = r.n_heads + 2 * r.n_kv_heads;
   const int N = heads * r.head_dim;
-  const long long total = (long long)M * heads * half;
+  const long long total = (long long)M * heads * groups;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(i % half);
-    const int head = (int)((i / half) % heads);
-    const int m = (int)(i / ((long long)half * heads));
-    const int c = head * r.head_dim + j;
-    float lo = scr[(size_t)m * N + c], hi = scr[(size_t)m * N + c + half];
-    scr[(size_t)m * N + c] = 0.f;
-    scr[(size_t)m * N + c + half] = 0.f;
+    const int j0 = (int)(i % groups) * 8;
+    const int head = (int)((i / groups) % heads);
+    const int m = (int)(i / ((long long)groups * heads));
+    const int c = head * r.head_dim + j0;
+    float* srow = scr + (size_t)m * N;
+    float lo[8], hi[8];
+    {
+      const float4 a0 = *reinterpret_cast<const float4*>(srow + c), a1 = *reinterpret_cast<const float4*>(srow + c + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(srow + c + half);
+      const float4 b1 = *reinterpret_cast<const float4*>(srow + c + half + 4);
+      lo[0] = a0.x; lo[1] = a0.y; lo[2] = a0.z; lo[3] = a0.w; lo[4] = a1.x; lo[5] = a1.y; lo[6] = a1.z; lo[7] = a1.w;
+      hi[0] = b0.x; hi[1] = b0.y; hi[2] = b0.z; hi[3] = b0.w; hi[4] = b1.x; hi[5] = b1.y; hi[6] = b1.z; hi[7] = b1.w;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(srow + c) = z;
+      *reinterpret_cast<float4*>(srow + c + 4) = z;
+      *reinterpret_cast<float4*>(srow + c + half) = z;
+      *reinterpret_cast<float4*>(srow + c + half + 4) = z;
+    }
     if (bias) {
-      lo += __bfloat162float(bias[c]);
-      hi += __bfloat162float(bias[c + half]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        lo[e] += __bfloat162float(bias[c + e]);
+        hi[e] += __bfloat162float(bias[c + half + e]);
+      }
     }
     const int pos = r.positions[m];
     const bool is_q = head < r.n_heads, is_k = !is_q && head < r.n_heads + r.n_kv_heads;
     if (is_q || is_k) {
-      const float2 cs = r.rope_cs[(size_t)pos * half + j];
-      const float a = lo, b = hi;
-      lo = a * cs.x - b * cs.y;
-      hi = b * cs.x + a * cs.y;
+      const float4* cs = reinterpret_cast<const float4*>(r.rope_cs + (size_t)pos * half + j0);
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        const float4 t = cs[e / 2];  // (cos, sin) x 2
+        const float a0 = lo[e], b0 = hi[e], a1 = lo[e + 1], b1 = hi[e + 1];
+        lo[e] = a0 * t.x - b0 * t.y;
+        hi[e] = b0 * t.x + a0 * t.y;
+        lo[e + 1] = a1 * t.z - b1 * t.w;
+        hi[e + 1] = b1 * t.z + a1 * t.w;
+      }
     }
     __nv_bfloat16* dst;
     if (is_q) {
       dst = q_out + (size_t)m * q_ld + head * r.head_dim;
     } else {
-      const int seq = r.row_seq[m];
-      const int page = r.block_tables[r.seq_bt_off[seq] + pos / r.page_size];
+      const int kv_row = r.row_kv[m];
+      const int page = kv_row / r.page_size, slot = kv_row - page * r.page_size;
       const int kvh = head - r.n_heads - (is_k ? 0 : r.n_kv_heads);
       dst = r.kv + (size_t)page * r.page_stride +
-            ((((size_t)r.layer * r.n_kv_heads + kvh) * 2 + (is_k ? 0 : 1)) * r.page_size + pos % r.page_size) * r.head_dim;
+            ((((size_t)r.layer * r.n_kv_heads + kvh) * 2 + (is_k ? 0 : 1)) * r.page_size + slot) * r.head_dim;
     }
-    dst[j] = __float2bfloat16(lo);
-    dst[j + half] = __float2bfloat16(hi);
+    st_global_v4(dst + j0, make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
+                                      pack_bf16(lo[6], lo[7])));
+    st_global_v4(dst + j0 + half, make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
+                                             pack_bf16(hi[6], hi[7])));
   }
 }
 
