@@ -76,6 +76,13 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict_
                                                         __nv_bfloat16* __restrict__ out, int d, float eps,
                                                         float* __restrict__ zero = nullptr, int zero_cols = 0) {
   constexpr int kMaxVec = 8192 / (4 * THREADS);
+  // the norm weights do not depend on the predecessor kernel: fetch them before the PDL wait
+  uint2 wv[kMaxVec];
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = (i * THREADS + threadIdx.x) * 4;
+    if (c < d) wv[i] = __ldg(reinterpret_cast<const uint2*>(w + c));
+  }
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
@@ -104,8 +111,7 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict_
   for (int i = 0; i < kMaxVec; ++i) {
     const int c = (i * THREADS + threadIdx.x) * 4;
     if (c < d) {
-      const uint2 wb = __ldg(reinterpret_cast<const uint2*>(w + c));
-      const float2 w01 = unpack_bf16(wb.x), w23 = unpack_bf16(wb.y);
+      const float2 w01 = unpack_bf16(wv[i].x), w23 = unpack_bf16(wv[i].y);
       uint2 pk;
       pk.x = pack_bf16(v[i].x * inv * w01.x, v[i].y * inv * w01.y);
       pk.y = pack_bf16(v[i].z * inv * w23.x, v[i].w * inv * w23.y);

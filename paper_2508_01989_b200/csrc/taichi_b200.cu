@@ -390,7 +390,14 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(N % 256 == 0, "gemm_ws: weight rows must be a multiple of 256");
   tc::GemmArgs args{};
-  const int n_tt = (M + 255) / 256;
+  // token tiles: the fewest that keep TN <= 256 (each extra tile re-reads the weights);
+  // TC_WS_NTT_RESID=n forces n for the residual GEMMs (measurement knob)
+  static const int ntt_resid = [] {
+    const char* e = std::getenv("TC_WS_NTT_RESID");
+    return e ? std::atoi(e) : 0;
+  }();
+  int n_tt = (M + 255) / 256;
+  if (epi == tc::EPI_RESID_F32 && ntt_resid > n_tt && (M + ntt_resid - 1) / ntt_resid >= 16) n_tt = ntt_resid;
   args.tn = ((M + n_tt - 1) / n_tt + 31) / 32 * 32;
   args.stages = tc::ws_stages(args.tn);
   args.M = M;
