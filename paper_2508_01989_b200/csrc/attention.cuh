@@ -367,9 +367,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   __shared__ uint32_t tmem_slot;
   const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int seq = p.qblk_seq[blockIdx.x];
-  const int qoff = p.qblk_off[blockIdx.x];
-  const int kvh = blockIdx.y;
+  // grid (kv heads, q blocks): all heads of the longest q block are dispatched first (the host
+  // sorts the q-block list longest-first)
+  const int seq = p.qblk_seq[blockIdx.y];
+  const int qoff = p.qblk_off[blockIdx.y];
+  const int kvh = blockIdx.x;
   const int q_start = p.seq_q_start[seq], q_len = p.seq_q_len[seq], pos0 = p.seq_pos0[seq];
   const int* bt = p.block_tables + p.seq_bt_off[seq];
   const int kv_end = pos0 + min(qoff + TT, q_len);

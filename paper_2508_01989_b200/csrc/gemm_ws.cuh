@@ -233,7 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
     if (args.trace) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      args.trace[blockIdx.x * 8 + i] = t;
+      args.trace[blockIdx.x * 16 + i] = t;
     }
   };
   if (threadIdx.x == 0) stamp(0);
@@ -402,6 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c0, r);
         tmem_ld_wait();
+        if (et == 0 && grp == 0 && ci < 6) stamp(8 + ci);      // 8, 10, 12: chunk's accumulator in registers
         if (ci == my_last) {  // this warp's last read of the accumulator: release it early
           tc_fence_before();
           __syncwarp();
@@ -429,6 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
           const int tok = w.mt * TN + c0 + t;
           if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
         }
+        if (et == 0 && grp == 0 && ci < 6) stamp(9 + ci);      // 9, 11, 13: chunk done
       }
       if (et == 0 && grp == 0) {
         if (local == 1) stamp(4);

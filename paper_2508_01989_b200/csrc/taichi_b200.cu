@@ -455,8 +455,8 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   static const bool trace = std::getenv("TC_WS_TRACE") != nullptr;
   unsigned long long* trace_dev = nullptr;
   if (trace) {
-    TC_CUDA(cudaMalloc(&trace_dev, (size_t)grid * 8 * 8));
-    TC_CUDA(cudaMemsetAsync(trace_dev, 0, (size_t)grid * 8 * 8, s));
+    TC_CUDA(cudaMalloc(&trace_dev, (size_t)grid * 16 * 8));
+    TC_CUDA(cudaMemsetAsync(trace_dev, 0, (size_t)grid * 16 * 8, s));
     args.trace = trace_dev;
   }
   CUtensorMap resid_map;
@@ -468,21 +468,21 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), args, epi, grid, s);
   TC_CUDA(cudaGetLastError());
   if (trace) {
-    std::vector<unsigned long long> h((size_t)grid * 8);
+    std::vector<unsigned long long> h((size_t)grid * 16);
     TC_CUDA(cudaMemcpyAsync(h.data(), trace_dev, h.size() * 8, cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     cudaFree(trace_dev);
     unsigned long long t0 = ~0ull;
     for (int b = 0; b < grid; ++b)
-      if (h[b * 8]) t0 = std::min(t0, h[b * 8]);
+      if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
     std::fprintf(stderr, "ws_trace M=%d N=%d K=%d epi=%d tn=%d units=%d splits=%d grid=%d (us from first entry: min/med/max)\n",
                  M, N, K, epi, args.tn, args.units, args.splits, grid);
-    const char* names[8] = {"entry", "prologue", "first_stage", "last_mma", "epi_first", "epi_last", "exit",
-                            "epi_start_last"};
-    for (int e = 0; e < 8; ++e) {
+    const char* names[14] = {"entry", "prologue", "first_stage", "last_mma", "epi_first", "epi_last", "exit",
+                             "epi_start_last", "c0_tmem", "c0_done", "c2_tmem", "c2_done", "c4_tmem", "c4_done"};
+    for (int e = 0; e < 14; ++e) {
       std::vector<double> v;
       for (int b = 0; b < grid; ++b)
-        if (h[b * 8 + e]) v.push_back((h[b * 8 + e] - t0) / 1e3);
+        if (h[b * 16 + e]) v.push_back((h[b * 16 + e] - t0) / 1e3);
       if (v.empty()) continue;
       std::sort(v.begin(), v.end());
       std::fprintf(stderr, "  %-12s %8.2f %8.2f %8.2f  (n=%zu)\n", names[e], v.front(), v[v.size() / 2], v.back(), v.size());
@@ -900,7 +900,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     TC_CUDA(cudaEventRecord(I->ev_fork, I->stream));
     launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
     TC_CUDA(cudaStreamWaitEvent(I->stream_pf, I->ev_fork, 0));
-    launch_k(tc::attn_prefill_tc<DH, G>, dim3(n_qblk, hk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
+    launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
              I->kv2_map, I->q_map, p);
     TC_CUDA(cudaEventRecord(I->ev_join, I->stream_pf));
     TC_CUDA(cudaStreamWaitEvent(I->stream, I->ev_join, 0));
@@ -912,7 +912,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
 #if TC_PREFILL_MMA_SYNC
     tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kPrefillThreads, tc::PrefillSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
 #else
-    launch_k(tc::attn_prefill_tc<DH, G>, dim3(n_qblk, hk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream,
+    launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream,
              I->kv2_map, I->q_map, p);
 #endif
     ++I->launches;
@@ -1037,6 +1037,23 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     row += sl.n_tokens;
     if (sl.want_logits) h[o_lrow + lr++] = row - 1;
+  }
+  if (qb > 1) {
+    // longest-first prefill work list (causal: later q blocks see more keys) so the CTAs that
+    // run on the few SMs left beside decode attention finish together
+    std::vector<std::pair<int, int>> order(qb);
+    for (int q = 0; q < qb; ++q) {
+      const tc_prefill_slice& sl = st->prefill[h[o_qbs + q]];
+      order[q] = {-(sl.pos0 + std::min(h[o_qbo + q] + tpc, sl.n_tokens)), q};
+    }
+    std::stable_sort(order.begin(), order.end());
+    std::vector<int32_t> qs(qb), qo(qb);
+    for (int q = 0; q < qb; ++q) {
+      qs[q] = h[o_qbs + order[q].second];
+      qo[q] = h[o_qbo + order[q].second];
+    }
+    std::copy(qs.begin(), qs.end(), h + o_qbs);
+    std::copy(qo.begin(), qo.end(), h + o_qbo);
   }
   for (int j = 0; j < n_dec; ++j) {
     const tc_decode_item& di = st->decode[j];
