@@ -318,7 +318,7 @@ def main():
     phases = {k: statistics.median(v) for k, v in phases.items()}
     # context: a decode-only step of the same decodes (half of all serving steps are decode-only,
     # SURVEY.md App. B); weight-streaming bound = weight bytes / HBM bandwidth
-    dec_ms = statistics.median([inst.step(decode=step_decode).gpu_ms for _ in range(5)])
+    dec_ms = statistics.median([inst.step(decode=step_decode).gpu_ms for _ in range(5)]) if D else float("nan")
     hbm, peak, peak_sus, peak_kind = measured_peaks()
     cost = step_cost(dims, P, prefix, D, ctx, n_logit)
     L = dims["n_layers"]
@@ -355,7 +355,7 @@ def main():
                 "config": config, "clocks": clocks.summary(),
                 "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches * world, "roofline": roofline, "step_roofline": step_roofline,
-                "decode_only_step": {"decode_reqs": D, "ctx": ctx, "ms": dec_ms, "tokens_per_s": D / dec_ms * 1e3,
+                "decode_only_step": None if not D else {"decode_reqs": D, "ctx": ctx, "ms": dec_ms, "tokens_per_s": D / dec_ms * 1e3,
                                      "weight_stream_bound_ms": 1e3 * sum(c["bytes"] for k, c in
                                                                          step_cost(dims, 0, 0, D, ctx, D).items()) /
                                                                (measured_peaks()[0] * 1e9)},

@@ -45,7 +45,20 @@ struct AttnParams {
   float* ws_o;               // [slot][G][DH] partial o of segments cut by CTA boundaries
   float* ws_ml;              // [slot][G][2]
   int* dec_cnt;              // [seg] arrival counters (zero; the last arriver resets)
+  int pf_poly;               // prefill softmax: share of exp2 on the FMA pipe (0 none, 1 = 1/4, 2 = 1/2)
 };
+
+// 2^x on the FMA/ALU pipes (offloads MUFU.EX2 in the prefill softmax): x = n + f, 2^f by a cubic
+// with max relative error 8.6e-5 (P is stored as bf16: 3.9e-3), exponent added as integer bits.
+TC_DEVICE float exp2_poly3(float x) {
+  x = fmaxf(x, -126.f);
+  const float n = floorf(x);
+  const float f = x - n;
+  float p = fmaf(f, 0.0770652f, 0.227647f);
+  p = fmaf(p, f, 0.69511634f);
+  p = fmaf(p, f, 1.f);
+  return __int_as_float(__float_as_int(p) + ((int)n << 23));
+}
 
 TC_DEVICE void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -548,7 +561,24 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const float base = m_used == -INFINITY ? 0.f : m_used;
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[32];
-      if (full) {
+      if (full && p.pf_poly == 2) {
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
+          const float p1 = exp2_poly3(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base));
+          sum4[x & 3] += p0 + p1;
+          pk[x] = pack_bf16(p0, p1);
+        }
+      } else if (full && p.pf_poly == 1) {
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
+          const float s1 = fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base);
+          const float p1 = (x & 1) ? exp2_poly3(s1) : fast_exp2(s1);
+          sum4[x & 3] += p0 + p1;
+          pk[x] = pack_bf16(p0, p1);
+        }
+      } else if (full) {
 #pragma unroll
         for (int x = 0; x < 32; ++x) {
           const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));

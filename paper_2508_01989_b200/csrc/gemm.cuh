@@ -84,6 +84,8 @@ struct GemmArgs {
   int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
   int stages;                // gemm_ws_2sm: smem ring depth for this token tile
   unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][8]
+  int dbg;                   // gemm_ws_2sm (tools only, TC_WS_DBG): 1 skip the row-phase stores,
+                             // 2 skip the row phase, 3 skip staging + row phase
   int streamk;               // gemm_ws_2sm, residual epilogue: pair p takes k-blocks
                              // [W p / P, W (p+1) / P) of the tile-major stream (W = tiles * kb)
 };

@@ -422,13 +422,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
             tma_reduce_add_2d(&map_o, smem_u32(sb), fbase, tok0);
             bulk_commit_group();
           }
-        } else {
+        } else if (args.dbg != 3) {
           asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");  // previous row phase done with sb
 #pragma unroll
           for (int i = 0; i < 32; ++i) sb[ws_stg_idx(i, fch) + fe] = __uint_as_float(r[i]);
           asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
           const int tok = w.mt * TN + c0 + t;
-          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
+          if (args.dbg == 1) {  // tools only: read the staged row, skip the global stores
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += ws_ld4(sb, t, s * 8 + q).x;
+            if (acc == 123456.f) args.trace[0] = 1;
+          } else if (args.dbg != 2 && tok < args.M) {
+            ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
+          }
         }
         if (et == 0 && grp == 0 && ci < 6) stamp(9 + ci);      // 9, 11, 13: chunk done
       }

@@ -436,6 +436,11 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     const char* e = std::getenv("TC_WS_STREAMK");
     return e ? std::atoi(e) : 1;
   }();
+  static const int ws_dbg = [] {
+    const char* e = std::getenv("TC_WS_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  args.dbg = ws_dbg;
   args.streamk = (epi == tc::EPI_RESID_F32 && force_splits == 0 &&
                   (streamk_mode == 2 || (streamk_mode == 1 && n_tt == 1 && tiles > pairs))) ? 1 : 0;
   if (args.streamk) {
@@ -1159,6 +1164,11 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   ap.ws_o = I->attn_ws_o;
   ap.dec_cnt = I->attn_cnt;
   ap.ws_ml = I->attn_ws_ml;
+  static const int pf_poly = [] {
+    const char* e = std::getenv("TC_PF_POLY");
+    return e ? std::atoi(e) : 0;
+  }();
+  ap.pf_poly = pf_poly;
   tc::QkvRopeArgs rp{};
   rp.kv = I->kv;
   rp.rope_cs = I->rope;
