@@ -527,12 +527,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 __global__ void finish_swiglu(float* __restrict__ scr, int M, int F, __nv_bfloat16* __restrict__ act) {
   pdl_wait();
   pdl_trigger();
-  const long long n4 = (long long)M * F / 4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i * 4;
-    const int m = (int)(e / F), j = (int)(e % F);
-    float* row = scr + (size_t)m * 2 * F;
-    const int gc = (j / 64) * 128 + (j % 64);
+  // grid (column blocks, rows): no 64-bit division in the index math (it dominated: 22 us per
+  // layer at 64 rows x 14336)
+  const int m = blockIdx.y;
+  float* row = scr + (size_t)m * 2 * F;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
+    const int gc = ((j >> 6) << 7) + (j & 63);
     const float4 g = *reinterpret_cast<const float4*>(row + gc);
     const float4 u = *reinterpret_cast<const float4*>(row + gc + 64);
     *reinterpret_cast<float4*>(row + gc) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -554,11 +554,11 @@ __global__ void finish_qkv_rope(float* __restrict__ scr, int M, QkvRopeArgs r, c
   const int half = r.head_dim / 2, groups = half / 8;
   const int heads = r.n_heads + 2 * r.n_kv_heads;
   const int N = heads * r.head_dim;
-  const long long total = (long long)M * heads * groups;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int j0 = (int)(i % groups) * 8;
-    const int head = (int)((i / groups) % heads);
-    const int m = (int)(i / ((long long)groups * heads));
+  // grid (blocks over heads x groups, rows): 32-bit index math only
+  const int m = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < heads * groups; i += gridDim.x * blockDim.x) {
+    const int j0 = (i % groups) * 8;
+    const int head = i / groups;
     const int c = head * r.head_dim + j0;
     float* srow = scr + (size_t)m * N;
     float lo[8], hi[8];

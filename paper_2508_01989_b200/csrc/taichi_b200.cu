@@ -1186,7 +1186,6 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   // decode-heavy steps: QKV / gate_up stream their weights over every SM (split-K, red.add into a
   // zeroed fp32 scratch) and a finish kernel applies RoPE + KV append / SwiGLU
   const bool streaming = T <= kStreamRows;
-  const int fin_blocks = 2 * I->sms;
   for (int l = 0; l < m.n_layers; ++l) {
     const LayerW& L = I->layers[l];
     {
@@ -1202,7 +1201,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.qkv, T, nullptr, I->qkv_n, nullptr, tc::EPI_BF16, I->sms, I->sk, s, 0, 0,
                                 nullptr, I->stream_scr);
-        launch_k(tc::finish_qkv_rope, fin_blocks, 256, 0, s, I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
+        launch_k(tc::finish_qkv_rope, dim3((I->qkv_n / 16 + 255) / 256, T), 256, 0, s, I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
                                                       I->qkv_n);
         ++I->launches;
       } else {
@@ -1231,7 +1230,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, nullptr, m.ffn_dim, nullptr, tc::EPI_BF16, I->sms, I->sk, s,
                                 0, 0, nullptr, I->stream_scr);
-        launch_k(tc::finish_swiglu, fin_blocks, 256, 0, s, I->stream_scr, T, m.ffn_dim, I->act);
+        launch_k(tc::finish_swiglu, dim3((m.ffn_dim / 4 + 255) / 256, T), 256, 0, s, I->stream_scr, T, m.ffn_dim, I->act);
         ++I->launches;
       } else {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
