@@ -86,6 +86,8 @@ struct GemmArgs {
   unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][8]
   int dbg;                   // gemm_ws_2sm (tools only, TC_WS_DBG): 1 skip the row-phase stores,
                              // 2 skip the row phase, 3 skip staging + row phase
+  // gemm_ws_2sm: plan of the next GEMM of the step (its first k-blocks are prefetched into L2)
+  int nx_on, nx_m_tiles, nx_splits, nx_kb, nx_units, nx_streamk, nx_pairs, nx_stages, nx_total;
   int streamk;               // gemm_ws_2sm, residual epilogue: pair p takes k-blocks
                              // [W p / P, W (p+1) / P) of the tile-major stream (W = tiles * kb)
 };

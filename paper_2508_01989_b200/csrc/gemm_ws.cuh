@@ -212,7 +212,7 @@ __device__ __forceinline__ bool ws_next(const GemmArgs& a, WsIter& it, int n_pai
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
     gemm_ws_2sm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                const __grid_constant__ CUtensorMap map_o, GemmArgs args) {
+                const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_next, GemmArgs args) {
   const int TN = args.tn, S = args.stages;
   const int stage_bytes = ws_stage_bytes(TN);
   extern __shared__ uint8_t smem_raw[];
@@ -305,6 +305,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
             phase ^= 1;
           }
         }
+      }
+      // all own loads issued: pull the next GEMM's first weight k-blocks for the same pair index
+      // into L2 (that kernel's pipeline fill then hits L2, not DRAM)
+      if (args.nx_on && pair < args.nx_pairs) {
+        int nt, k0, k1;
+        if (args.nx_streamk) {  // the pair's range of the tile-major k-block stream (ws_iter_begin)
+          const long long pos = (long long)args.nx_total * pair / args.nx_pairs;
+          const int tile = (int)(pos / args.nx_kb);
+          nt = tile / args.nx_m_tiles;
+          k0 = (int)(pos - (long long)tile * args.nx_kb);
+          k1 = min(args.nx_kb, k0 + args.nx_stages);
+        } else {
+          GemmArgs nx = args;
+          nx.m_tiles = args.nx_m_tiles;
+          nx.splits = args.nx_splits;
+          nx.kb = args.nx_kb;
+          const Unit u0 = unit_of(nx, pair);
+          nt = u0.nt;
+          k0 = u0.k0;
+          k1 = min(u0.k1, u0.k0 + args.nx_stages);
+        }
+        for (int kb = k0; nt >= 0 && kb < k1; ++kb) tma_prefetch_2d_l2(&map_next, kb * kGemmBK, nt * 256 + wrow);
       }
     }
   } else if (warp == 1) {

@@ -371,24 +371,31 @@ bool ws_enabled() {
   return on;
 }
 
-void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensorMap& mo, const tc::GemmArgs& args,
-                    int epi, int grid, cudaStream_t s) {
+void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensorMap& mo, const CUtensorMap& mn,
+                    const tc::GemmArgs& args, int epi, int grid, cudaStream_t s) {
   const int smem = tc::kWsSmemBytes;
   switch (epi) {
-    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
-    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
+    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
+    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
+    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
+    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
+    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
     default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
 
-int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi, int sms,
-                cudaStream_t s, int force_splits, const tc::QkvRopeArgs* rope, const CUtensorMap* out_map) {
-  const int N = (int)w.rows, K = (int)w.cols;
-  TC_REQUIRE(N % 256 == 0, "gemm_ws: weight rows must be a multiple of 256");
+// The GEMM that follows in the step (its weights' first k-blocks are pulled into L2 by the
+// current GEMM's producer once it has issued its own loads: the next kernel's pipeline fill then
+// comes from L2 instead of DRAM).
+struct NextGemm {
+  const WMat* w = nullptr;
+  int M = 0, epi = 0;
+};
+
+// Tiling / split / stream-K plan of a weight-stationary GEMM (shared by the launch and by the
+// previous GEMM's L2 prefetch of this one).
+tc::GemmArgs plan_gemm_ws(int M, int N, int K, int epi, int sms, int force_splits) {
   tc::GemmArgs args{};
   // token tiles: the fewest that keep TN <= 256 (each extra tile re-reads the weights);
   // TC_WS_NTT_RESID=n forces n for the residual GEMMs (measurement knob)
@@ -447,6 +454,35 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     args.splits = 1;
     args.units = (int)std::min<long long>(pairs, tiles * args.kb);  // one k-block range per pair
   }
+  return args;
+}
+
+int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi, int sms,
+                cudaStream_t s, int force_splits, const tc::QkvRopeArgs* rope, const CUtensorMap* out_map,
+                const NextGemm* next = nullptr) {
+  const int N = (int)w.rows;
+  TC_REQUIRE(N % 256 == 0, "gemm_ws: weight rows must be a multiple of 256");
+  const int pairs = sms / 2;
+  tc::GemmArgs args = plan_gemm_ws(M, N, (int)w.cols, epi, sms, force_splits);
+  // off by default: measured -0.5% (mixed) / -1.7% (decode-only) -- the fill is not DRAM-bound
+  static const bool l2_next = [] {
+    const char* e = std::getenv("TC_WS_PF_NEXT");
+    return e && e[0] == '1';
+  }();
+  const CUtensorMap* next_map = &w.map(128);
+  if (l2_next && next && next->w && next->w->rows % 256 == 0) {
+    const tc::GemmArgs nx = plan_gemm_ws(next->M, (int)next->w->rows, (int)next->w->cols, next->epi, sms, 0);
+    args.nx_on = 1;
+    args.nx_m_tiles = nx.m_tiles;
+    args.nx_splits = nx.splits;
+    args.nx_kb = nx.kb;
+    args.nx_units = nx.units;
+    args.nx_streamk = nx.streamk;
+    args.nx_pairs = (int)std::min<long long>(pairs, nx.units);
+    args.nx_stages = nx.stages;
+    args.nx_total = nx.m_tiles * nx.n_tiles * nx.kb;
+    next_map = &next->w->map(128);
+  }
   args.out = out;
   args.ldo = ldo;
   args.bias = bias;
@@ -470,7 +506,8 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     TC_REQUIRE(ldo == N, "gemm_ws: residual output must be dense [M, N]");
     resid_map = out_map ? *out_map : make_resid_map(out, (uint64_t)M, (uint64_t)N);
   }
-  launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), args, epi, grid, s);
+  launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), *next_map, args, epi,
+                 grid, s);
   TC_CUDA(cudaGetLastError());
   if (trace) {
     std::vector<unsigned long long> h((size_t)grid * 16);
@@ -481,7 +518,7 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     for (int b = 0; b < grid; ++b)
       if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
     std::fprintf(stderr, "ws_trace M=%d N=%d K=%d epi=%d tn=%d units=%d splits=%d grid=%d (us from first entry: min/med/max)\n",
-                 M, N, K, epi, args.tn, args.units, args.splits, grid);
+                 M, N, args.K, epi, args.tn, args.units, args.splits, grid);
     const char* names[14] = {"entry", "prologue", "first_stage", "last_mma", "epi_first", "epi_last", "exit",
                              "epi_start_last", "c0_tmem", "c0_done", "c2_tmem", "c2_done", "c4_tmem", "c4_done"};
     for (int e = 0; e < 14; ++e) {
@@ -499,7 +536,8 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
 // out = epi(A[M,K] * W[N,K]^T). a: the activation buffer's maps.
 int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
              int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
-             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr, const CUtensorMap* out_map = nullptr) {
+             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr, const CUtensorMap* out_map = nullptr,
+             const NextGemm* next = nullptr) {
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(K % 64 == 0, "gemm: K must be a multiple of 64");
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
@@ -514,8 +552,8 @@ int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfl
     // streaming mode (decode-only steps): split-K partials land in the zeroed fp32 scratch via
     // TMA bulk adds; the finish kernel applies RoPE + KV append / SwiGLU
     if (red_out != nullptr) return run_gemm_ws(a, w, M, red_out, N, nullptr, tc::EPI_RESID_F32, sms, s, force_splits,
-                                               nullptr, nullptr);
-    return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map);
+                                               nullptr, nullptr, next);
+    return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map, next);
   }
   const CUtensorMap& a_map = a.m128;
   const bool two_sm = N % 256 == 0 && (force_bn == 512 || (force_bn == 0 && M > kGemm2MinM));
@@ -1186,6 +1224,14 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   // decode-heavy steps: QKV / gate_up stream their weights over every SM (split-K, red.add into a
   // zeroed fp32 scratch) and a finish kernel applies RoPE + KV append / SwiGLU
   const bool streaming = T <= kStreamRows;
+  // plan of the GEMM that follows (its weights' first k-blocks are prefetched into L2)
+  auto next_gemm = [&](const WMat* w, int epi_full) {
+    NextGemm n;
+    n.w = w;
+    n.M = T;
+    n.epi = streaming && (epi_full == tc::EPI_QKV_ROPE || epi_full == tc::EPI_SWIGLU) ? tc::EPI_RESID_F32 : epi_full;
+    return n;
+  };
   for (int l = 0; l < m.n_layers; ++l) {
     const LayerW& L = I->layers[l];
     {
@@ -1198,15 +1244,16 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       // QKV projection with fused bias, RoPE and paged KV append (q stays in I->qkv)
       ProfScope p_(I, "gemm_qkv");
       rp.layer = l;
+      const NextGemm nx_o = next_gemm(&L.o, tc::EPI_RESID_F32);
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.qkv, T, nullptr, I->qkv_n, nullptr, tc::EPI_BF16, I->sms, I->sk, s, 0, 0,
-                                nullptr, I->stream_scr);
+                                nullptr, I->stream_scr, nullptr, &nx_o);
         launch_k(tc::finish_qkv_rope, dim3((I->qkv_n / 16 + 255) / 256, T), 256, 0, s, I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
                                                       I->qkv_n);
         ++I->launches;
       } else {
         I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
-                                tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp);
+                                tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp, nullptr, nullptr, &nx_o);
       }
     }
     {
@@ -1216,8 +1263,9 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_o");
+      const NextGemm nx_gu = next_gemm(&L.gate_up, tc::EPI_SWIGLU);
       I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
-                              nullptr, nullptr, &I->map_resid);
+                              nullptr, nullptr, &I->map_resid, &nx_gu);
     }
     {
       ProfScope p_(I, "norm");
@@ -1227,19 +1275,22 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_gate_up");
+      const NextGemm nx_down = next_gemm(&L.down, tc::EPI_RESID_F32);
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, nullptr, m.ffn_dim, nullptr, tc::EPI_BF16, I->sms, I->sk, s,
-                                0, 0, nullptr, I->stream_scr);
+                                0, 0, nullptr, I->stream_scr, nullptr, &nx_down);
         launch_k(tc::finish_swiglu, dim3((m.ffn_dim / 4 + 255) / 256, T), 256, 0, s, I->stream_scr, T, m.ffn_dim, I->act);
         ++I->launches;
       } else {
-        I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
+        I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s,
+                                0, 0, nullptr, nullptr, nullptr, &nx_down);
       }
     }
     {
       ProfScope p_(I, "gemm_down");
+      const NextGemm nx_qkv = l + 1 < m.n_layers ? next_gemm(&I->layers[l + 1].qkv, tc::EPI_QKV_ROPE) : NextGemm{};
       I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
-                              nullptr, nullptr, &I->map_resid);
+                              nullptr, nullptr, &I->map_resid, &nx_qkv);
     }
   }
   if (n_logit > 0) {
