@@ -134,7 +134,9 @@ class GpuExecutor final : public pdsim::StepExecutor {
     ++stats_.migrations;
     stats_.copy_ms += ms;
     stats_.copy_bytes += bytes;
-    held_[static_cast<size_t>(from)].erase(rid);  // a token sampled mid-flight is discarded
+    // A token sampled by an in-flight step on `from` stays held: the engine commits it only if the
+    // request is resident on `from` again when that step completes (it can flow away and back
+    // within one step: degrade, then backflow), and the next join on `from` overwrites it.
     if (mode_ == ClockMode::Logical) return model_ms;
     const bool same_dev = !devices_.empty() && devices_[static_cast<size_t>(from)] == devices_[static_cast<size_t>(to)];
     if (same_dev && link_gbps_ > 0.0) return static_cast<double>(bytes) / (link_gbps_ * 1e6);
