@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--pool-tokens", type=int, default=0)
     ap.add_argument("--n-requests", type=int, default=0)
     ap.add_argument("--profile", default="", help="calibration JSON whose 'profile' replaces the config's")
+    ap.add_argument("--slo", default="", help="TTFT_ms,TPOT_ms override of the config's SLO (config-4 SLO sets)")
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
     base = json.loads(pathlib.Path(args.base).read_text())
@@ -49,6 +50,9 @@ def main():
         base["profile"] = json.loads(pathlib.Path(args.profile).read_text())["profile"]
     if args.n_requests:
         base["workload"]["n_requests"] = args.n_requests
+    if args.slo:
+        ttft, tpot = (float(x) for x in args.slo.split(","))
+        base["slo"]["ttft_ms"], base["slo"]["tpot_ms"] = ttft, tpot
     target = base["slo"].get("attainment_target", 0.9)
     grid = [float(q) for q in args.qps.split(",")]
     seeds = [int(s) for s in args.seeds.split(",")]
