@@ -128,8 +128,9 @@ tc_status tc_kv_release(tc_instance* inst, int64_t req_id);
 /* Pages currently held by req_id (0 if none) and free pages in the pool. */
 tc_status tc_kv_stats(tc_instance* inst, int64_t req_id, int64_t* req_pages, int64_t* free_pages);
 
-/* Move the first n_tokens KV rows of req_id from src to dst (pages on dst are
- * allocated, src pages freed once the copy is ordered on src's stream). The copy
+/* Move the KV of req_id from src to dst: every page src holds for it (at least the first n_tokens
+ * rows; a step in flight on src may have written one more row) -- pages on dst are allocated, src
+ * pages freed once the copy is ordered on src's stream. The copy
  * runs on src's stream after its in-flight step and pushes over NVLink when the
  * instances are on different GPUs; dst's next step waits for it. *copy_ms (may be
  * NULL) receives the device time of the copy after tc_kv_migrate_wait. */

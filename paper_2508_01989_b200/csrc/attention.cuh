@@ -657,13 +657,13 @@ constexpr int kDecConsumers = 4;
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 constexpr int kDecRingBytes = 192 * 1024;
 
-template <int DH, int G>
+template <int DH, int G, int RING = kDecRingBytes>
 struct DecodeSmem {
   static constexpr int kStageBytes = KvBlock<DH>::kPairBytes;  // one page-head: K block then V block
-  static constexpr int kStages = kDecRingBytes / kStageBytes;
+  static constexpr int kStages = RING / kStageBytes;
   static constexpr int kQBytes = G * DH * 2;
   static constexpr int kPartFloats = kDecConsumers * G * DH;  // per buffer
-  static constexpr int kOffQ = kDecRingBytes;
+  static constexpr int kOffQ = RING;
   static constexpr int kOffPart = kOffQ + 2 * ((kQBytes + 127) / 128 * 128);
   static constexpr int kOffMl = kOffPart + 2 * kPartFloats * 4;
   static constexpr int kBytes = kOffMl + 2 * kDecConsumers * G * 2 * 4 + 1024;
@@ -729,9 +729,11 @@ TC_DEVICE void store_out_row(__nv_bfloat16* out_row, const float (&acc)[G][DH / 
   }
 }
 
-template <int DH, int G>
-__global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  using SM = DecodeSmem<DH, G>;
+// RING < 192 KB: smaller ring, two CTAs per SM (twice the consumer warps per SM; A/B TC_DEC_2CTA)
+template <int DH, int G, int RING = kDecRingBytes>
+__global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
+    attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  using SM = DecodeSmem<DH, G, RING>;
   constexpr int S = SM::kStages;
   constexpr int V = DH / 32;
   extern __shared__ uint8_t attn_smem_raw[];

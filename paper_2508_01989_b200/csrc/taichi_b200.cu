@@ -208,6 +208,8 @@ void init_kernel_attrs(int dev) {
   attr((const void*)tc::attn_prefill_tc<128, 5>, tc::PfCfg<128, 5>::kBytes);
   attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64, 2>::kBytes);
   attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128, 4>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 96 * 1024>, tc::DecodeSmem<128, 4, 96 * 1024>::kBytes);
+  attr((const void*)tc::attn_decode<128, 5, 96 * 1024>, tc::DecodeSmem<128, 5, 96 * 1024>::kBytes);
   attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128, 5>::kBytes);
   done.insert(dev);
 }
@@ -934,6 +936,14 @@ struct ProfScope {
   }
 };
 
+bool dec_2cta() {
+  static const bool on = [] {
+    const char* e = std::getenv("TC_DEC_2CTA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int DH, int G>
 void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int hk = I->d.n_kv_heads;
@@ -941,7 +951,11 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     // decode on the main stream over sms - pf_sms CTAs (launched first, so its persistent CTAs
     // take their SMs), prefill beside it on stream_pf over whatever SMs remain; join before O
     TC_CUDA(cudaEventRecord(I->ev_fork, I->stream));
-    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    if (dec_2cta() && DH == 128)
+      launch_k(tc::attn_decode<DH, G, 96 * 1024>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G, 96 * 1024>::kBytes,
+               I->stream, I->kv_map, p);
+    else
+      launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
     TC_CUDA(cudaStreamWaitEvent(I->stream_pf, I->ev_fork, 0));
     launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
              I->kv2_map, I->q_map, p);
@@ -961,7 +975,11 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     ++I->launches;
   }
   if (n_dec > 0) {
-    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    if (dec_2cta() && DH == 128)
+      launch_k(tc::attn_decode<DH, G, 96 * 1024>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G, 96 * 1024>::kBytes,
+               I->stream, I->kv_map, p);
+    else
+      launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
     ++I->launches;
   }
   TC_CUDA(cudaGetLastError());
@@ -1039,7 +1057,8 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     I->pf_sms = std::max(0, std::min({want, n_qblk * m.n_kv_heads, I->sms / 2}));
   }
   const int dec_sms = I->sms - I->pf_sms;
-  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_sms, (W + 7) / 8)) : 0;
+  const int dec_ctas = (dec_2cta() && m.head_dim == 128) ? 2 * dec_sms : dec_sms;
+  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_ctas, (W + 7) / 8)) : 0;
   // entries: one per (CTA, segment overlap); at most n_seg + dec_grid
   const int max_entries = n_seg + dec_grid;
   // layout of the metadata block
@@ -1373,10 +1392,14 @@ void migrate(tc_instance* src, tc_instance* dst, int64_t req, int64_t n_tokens) 
   TC_REQUIRE(dst->tables.find(req) == dst->tables.end() || dst->tables[req].empty(),
              "migrate: request already has KV on destination");
   const int ps = src->desc.page_size;
-  const int64_t np = (n_tokens + ps - 1) / ps;
-  TC_REQUIRE(np <= (int64_t)it->second.size(), "migrate: source holds fewer pages than requested");
+  // Every page the source holds moves (at least the n_tokens rows asked for): a step still in
+  // flight on the source may have written the next row into a page beyond n_tokens, and a request
+  // that flows away and back within that step must bring that row home (engine.hpp:461-493
+  // commits the step's token if the request is resident again when the step completes).
+  TC_REQUIRE((n_tokens + ps - 1) / ps <= (int64_t)it->second.size(), "migrate: source holds fewer pages than requested");
+  const int64_t np = (int64_t)it->second.size();
   TC_REQUIRE(2 * np <= src->mig_cap, "migrate: request too long");
-  ensure_pages(dst, req, n_tokens);
+  ensure_pages(dst, req, np * ps);
   const std::vector<int32_t>& dp = dst->tables[req];
   for (int64_t i = 0; i < np; ++i) {
     src->mig_host[i] = it->second[i];

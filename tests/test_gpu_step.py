@@ -209,6 +209,38 @@ def test_tiny_migration_between_instances(tiny):
     dst.close()
 
 
+def test_migration_round_trip_during_inflight_step(tiny):
+    """A request degrades and back-flows while a step that decodes it is still in flight on the
+    source (the engine then commits that step's token, engine.hpp:461-493). Whole held pages move,
+    so the row the in-flight step writes (here the first row of a fresh page) survives the round
+    trip and decoding continues on the exact greedy trajectory."""
+    from paper_2508_01989_b200 import Instance
+    src, model = tiny
+    dst = Instance("tiny", weight_seed=11, kv_pool_tokens=1 << 14, max_step_tokens=512, max_seqs=16, max_context=4096)
+    rid = 78
+    prompt = mr.prompt_tokens(11, rid, 32, 1024)  # footprint 33: the next row (32) opens page 3
+    out = src.step(prefill=[(rid, 0, prompt, True)])
+    f = Follower(model, prompt)
+    f.check(int(out.sampled[0]))
+    tok, pos = int(out.sampled[0]), len(prompt)
+    src.launch(decode=[(rid, pos, tok)])       # writes row 32, not yet waited
+    src.migrate_to(dst, rid, pos)              # degrade: footprint - 1 rows requested
+    src.migrate_wait()
+    dst.migrate_to(src, rid, pos)              # backflow before the step completes
+    dst.migrate_wait()
+    o = src.wait()
+    f.feed([tok])
+    f.check(int(o.sampled[0]))
+    tok, pos = int(o.sampled[0]), pos + 1
+    for _ in range(4):
+        f.feed([tok])
+        o = src.step(decode=[(rid, pos, tok)], keep_logits=True)
+        f.check(int(o.sampled[0]), o.logits[0])
+        tok, pos = int(o.sampled[0]), pos + 1
+    src.kv_release(rid)
+    dst.close()
+
+
 @pytest.fixture(scope="module")
 def llama_l2():
     from paper_2508_01989_b200 import Instance
