@@ -46,6 +46,7 @@ struct AttnParams {
   float* ws_ml;              // [slot][G][2]
   int* dec_cnt;              // [seg] arrival counters (zero; the last arriver resets)
   int pf_poly;               // prefill softmax: share of exp2 on the FMA pipe (0 none, 1 = 1/4, 2 = 1/2)
+  int dec_l2_ahead;          // decode producer prefetches the next 32 pages of an entry into L2
 };
 
 // 2^x on the FMA/ALU pipes (offloads MUFU.EX2 in the prefill softmax): x = n + f, 2^f by a cubic
@@ -82,6 +83,12 @@ TC_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, 
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
+}
+// L2-only prefetch of one 3-D box (deepens the decode page stream beyond the smem ring).
+TC_DEVICE void tma_prefetch_3d_l2(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
 }
 TC_DEVICE void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -785,6 +792,10 @@ __global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
         for (int c = pg0; c < pg1; c += 32) {
           // lane j: pool row of page c + j (coordinates computed 32 at a time, off the issue path)
           const int row = c + lane < pg1 ? kv_row(p, p.block_tables[bt_off + c + lane], kvh) : 0;
+          // the entry's next 32 pages into L2 (one prefetch per lane): keeps ~2x the ring's bytes
+          // in flight per SM, the decode stream being bound by per-SM outstanding bytes
+          if (p.dec_l2_ahead && c + 32 + lane < pg1)
+            tma_prefetch_3d_l2(&kv_map, KV_COORD(kv_row(p, p.block_tables[bt_off + c + 32 + lane], kvh)));
           const int n = min(32, pg1 - c);
           for (int j = 0; j < n; ++j, ++g) {
             const int rj = __shfl_sync(0xffffffffu, row, j);

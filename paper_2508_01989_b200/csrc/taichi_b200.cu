@@ -1226,6 +1226,11 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     return e ? std::atoi(e) : 0;
   }();
   ap.pf_poly = pf_poly;
+  static const int dec_l2 = [] {
+    const char* e = std::getenv("TC_DEC_L2");
+    return e ? std::atoi(e) : 1;
+  }();
+  ap.dec_l2_ahead = dec_l2;
   tc::QkvRopeArgs rp{};
   rp.kv = I->kv;
   rp.rope_cs = I->rope;
