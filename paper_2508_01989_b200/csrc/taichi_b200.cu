@@ -1034,10 +1034,13 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   const int n_seg = n_dec * m.n_kv_heads;
   long long W = 0;
   for (int i = 0; i < n_dec; ++i) W += (long long)(st->decode[i].pos / ps + 1) * m.n_kv_heads;
-  // Mixed steps run prefill attention beside decode attention (pf_sms SMs left to prefill).
-  // Balance: prefill CTA-time ~ 2.5 us per 128-key tile per CTA (B200, Llama-3-8B shapes; the
-  // measured optimum at P=512 over a 512 prefix + 64 decodes @1k is 40 SMs) over
-  // pf_sms SMs vs decode at ~5.2 TB/s over the rest. TC_PF_SMS overrides (0 = serial).
+  // Mixed steps run prefill attention beside decode attention (pf_sms SMs left to prefill; the
+  // prefill CTAs spill onto every SM once the persistent decode CTAs finish). Model: decode moves
+  // its K/V at ~40 GB/s per SM up to ~5.2 TB/s; prefill costs ~2.5 us per 128-key tile + 4 us per CTA;
+  // step attention time(P) = T_dec(sms - P) + max(0, W_pf - P * T_dec) / sms. The curve is flat
+  // near its minimum; take the smallest P within 0.5% of it, plus 4 (measured optima: Llama-3-8B
+  // P=512 over 512 + 64 decodes @1k: 32-40, flat; Qwen2.5-14B 1024 over 4096 + 32 @8k: 24).
+  // TC_PF_SMS overrides (0 = serial).
   I->pf_sms = 0;
   if (n_dec > 0 && n_qblk > 0) {
     long long pf_tiles = 0;
@@ -1046,9 +1049,22 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       for (int q = 0; q < sl.n_tokens; q += tpc) pf_tiles += (sl.pos0 + std::min(q + tpc, sl.n_tokens) + 127) / 128;
     }
     pf_tiles *= m.n_kv_heads;
-    const double pf_cta_us = 2.5 * (double)pf_tiles * (m.head_dim / 128.0);
-    const double dec_us = (double)W * ps * m.head_dim * 2 * 2 / 5.2e6;  // K + V bytes / (5.2 TB/s)
-    int want = (int)std::ceil(pf_cta_us / std::max(dec_us, 1.0));
+    // CTA-us: ~2.5 us per 128-key tile plus ~4 us fixed per CTA (Q load, TMEM, epilogue)
+    const double w_pf = (2.5 * (double)pf_tiles + 4.0 * n_qblk * m.n_kv_heads) * (m.head_dim / 128.0);
+    const double dec_bytes = (double)W * ps * m.head_dim * 2 * 2;
+    auto t_of = [&](int P) {
+      const double t_dec = dec_bytes / std::min((I->sms - P) * 40e3, 5.2e6);  // us (bytes / (bytes per us))
+      return t_dec + std::max(0.0, w_pf - P * t_dec) / I->sms;
+    };
+    const int p_max = std::min(n_qblk * m.n_kv_heads, I->sms / 2);
+    double t_min = 1e30;
+    for (int P = 4; P <= p_max; P += 4) t_min = std::min(t_min, t_of(P));
+    int want = 0;
+    for (int P = 4; P <= p_max; P += 4)
+      if (t_of(P) <= 1.005 * t_min) {
+        want = std::min(P + 4, p_max);
+        break;
+      }
     static const int env_pf = [] {
       const char* e = std::getenv("TC_PF_SMS");
       return e ? std::atoi(e) : -1;
