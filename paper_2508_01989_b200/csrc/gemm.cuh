@@ -84,6 +84,7 @@ struct GemmArgs {
   int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
   int stages;                // gemm_ws_2sm: smem ring depth for this token tile
   unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][8]
+  int rope_stage;            // gemm_ws_2sm QKV epilogue: stage (cos, sin) rows in the idle ring
   int dbg;                   // gemm_ws_2sm (tools only, TC_WS_DBG): 1 skip the row-phase stores,
                              // 2 skip the row phase, 3 skip staging + row phase
   // gemm_ws_2sm: plan of the next GEMM of the step (its first k-blocks are prefetched into L2)

@@ -57,7 +57,7 @@ __device__ __forceinline__ float4 ws_ld4(const float* sb, int t, int ch) {
 // starting at global weight row fbase.
 template <int EPI>
 __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const float* sb, int t, int s, int tok, int fbase,
-                                                int pos, int kv_row) {
+                                                int pos, int kv_row, const float2* cs_stage = nullptr) {
   if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_BIAS) {
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)tok * args.ldo + fbase + s * 32;
 #pragma unroll
@@ -145,7 +145,8 @@ __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const floa
       }
     }
     if (is_q || is_k) {
-      const float2* cs = r.rope_cs + (size_t)pos * half + j0;
+      // (cos, sin) of this row: staged in smem by the epilogue (single-unit launches) or global
+      const float2* cs = cs_stage ? cs_stage + j0 : r.rope_cs + (size_t)pos * half + j0;
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {
         const float4 c = *reinterpret_cast<const float4*>(cs + i);  // (cos, sin) x 2
@@ -410,6 +411,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (et == 0 && grp == 0) stamp(7);
+      // single-unit launch (every pair owns one unit, e.g. QKV at T=576): the MMAs are done and the
+      // ring is idle, so stage this unit's (cos, sin) rows in it with one round of independent 16 B
+      // loads instead of one dependent L2 round trip per 32-token chunk
+      const float2* cs_stage = nullptr;
+      if constexpr (EPI == EPI_QKV_ROPE) {
+        if (args.rope_stage) {
+          const int half = args.rope.head_dim >> 1, cpr = half / 2;  // 16 B chunks per row
+          float4* dst = reinterpret_cast<float4*>(smem);
+          const int e2 = threadIdx.x - 128;
+          for (int k = e2; k < TN * cpr; k += 256) {
+            const int tl = k / cpr, c = k - tl * cpr;
+            if (w.mt * TN + tl < args.M)
+              dst[k] = __ldg(reinterpret_cast<const float4*>(args.rope.rope_cs + (size_t)mpos[tl] * half) + c);
+          }
+          asm volatile("bar.sync 3, 256;" ::: "memory");
+          cs_stage = reinterpret_cast<const float2*>(smem);
+        }
+      }
       const int fbase = w.nt * 256 + (int)rank * 128;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
       const int my_last = (n_chunks - 1 - grp) >= 0 ? ((n_chunks - 1 - grp) & ~1) + grp : -1;
@@ -456,7 +475,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
             for (int q = 0; q < 8; ++q) acc += ws_ld4(sb, t, s * 8 + q).x;
             if (acc == 123456.f) args.trace[0] = 1;
           } else if (args.dbg != 2 && tok < args.M) {
-            ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
+            ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t],
+                                 cs_stage ? cs_stage + (size_t)(c0 + t) * (args.rope.head_dim >> 1) : nullptr);
           }
         }
         if (et == 0 && grp == 0 && ci < 6) stamp(9 + ci);      // 9, 11, 13: chunk done

@@ -492,6 +492,15 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
     TC_REQUIRE(128 % rope->head_dim == 0, "gemm_ws: a 128-row half tile must cover whole heads");
     args.rope = *rope;
+    // off: measured slower (qkv 1.17 -> 1.55 ms per step): the 96 KB per CTA staging burst costs
+    // more than the per-chunk table loads it removes
+    static const bool rope_stage_on = [] {
+      const char* e = std::getenv("TC_WS_ROPE_SMEM");
+      return e && e[0] == '1';
+    }();
+    // every pair owns exactly one unit -> its ring is idle during the epilogue
+    args.rope_stage = rope_stage_on && args.units <= pairs && !args.streamk &&
+                      (size_t)args.tn * (rope->head_dim / 2) * 8 <= (size_t)args.stages * tc::ws_stage_bytes(args.tn);
   }
   const int grid = 2 * (int)std::min<long long>(pairs, args.units);
   // TC_WS_TRACE=1 (tools only): per-CTA %globaltimer timeline of this launch printed to stderr
