@@ -28,9 +28,14 @@
 
 #include "gemm.cuh"
 
+#ifndef TC_WS_MAX_STAGES
+#define TC_WS_MAX_STAGES 12
+#endif
+
 namespace tc {
 
-constexpr int kWsMaxStages = 8;
+constexpr int kWsMaxStages = TC_WS_MAX_STAGES;  // ring depth cap (barrier area fits 12)
+static_assert(kWsMaxStages <= 12, "ws GEMM barrier area holds at most 12 stages");
 constexpr int kWsWBytes = 128 * kGemmBK * 2;           // this CTA's 128 weight rows per k-block
 constexpr int kWsStagingFloats = 32 * 128;             // one 32-token x 128-feature fp32 chunk
 constexpr int kWsSmemBytes = 232448;                   // max dynamic shared memory per CTA (sm_100)
