@@ -9,7 +9,7 @@
  *                                   IterationComplete handler engine.hpp:461
  *                                   (wait + read back sampled token ids);
  *                                   cost_model.hpp:43-53.
- *   tc_kv_migrate                   replaces transfer_time_ms at engine.hpp:402
+ *   tc_kv_migrate(_async)           replaces transfer_time_ms at engine.hpp:402
  *                                   (degrade/backflow, full footprint) and
  *                                   engine.hpp:516 (init, prompt_len tokens);
  *                                   cost_model.hpp:81-85.
@@ -66,12 +66,16 @@ typedef struct {
   tc_model_dims dims;
   uint64_t weight_seed;      /* deterministic random init (see tc_weight_value) */
   int32_t page_size;         /* tokens per KV page (16) */
-  int64_t kv_pool_tokens;    /* physical KV capacity in tokens (rounded up to pages) */
+  int64_t kv_pool_tokens;    /* physical KV capacity in tokens (rounded up to pages); <= 0: every
+                                free byte of HBM but a 4 GiB reserve */
   int32_t max_step_tokens;   /* max packed rows per step (prefill + decode) */
   int32_t max_seqs;          /* max sequences (slices + decodes) per step */
   int32_t max_context;       /* max position + 1 (RoPE table size) */
   const struct tc_instance* share_weights; /* optional: reuse this instance's weights (same device,
                                               dims and seed) -- several instances on one GPU */
+  const struct tc_instance* share_kv_pool; /* optional: draw KV pages from this instance's pool (same
+                                              device and KV geometry; kv_pool_tokens is then ignored):
+                                              co-located instances share one HBM budget */
 } tc_instance_desc;
 
 tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out);
@@ -115,6 +119,7 @@ typedef struct {
   int32_t launches;       /* kernels this library launched for the step */
   int64_t h2d_bytes;      /* host->device bytes copied for the step (token ids + metadata) */
   int64_t d2h_bytes;      /* device->host bytes read back (sampled ids [+ logits]) */
+  int32_t attn_pf_sms;    /* SMs given to prefill attention beside decode attention (0 = serial) */
 } tc_step_result;
 
 /* Enqueue a step (asynchronous); pages for new positions are allocated here. */
@@ -128,14 +133,28 @@ tc_status tc_kv_release(tc_instance* inst, int64_t req_id);
 /* Pages currently held by req_id (0 if none) and free pages in the pool. */
 tc_status tc_kv_stats(tc_instance* inst, int64_t req_id, int64_t* req_pages, int64_t* free_pages);
 
-/* Move the KV of req_id from src to dst: every page src holds for it (at least the first n_tokens
- * rows; a step in flight on src may have written one more row) -- pages on dst are allocated, src
- * pages freed once the copy is ordered on src's stream. The copy
- * runs on src's stream after its in-flight step and pushes over NVLink when the
- * instances are on different GPUs; dst's next step waits for it. *copy_ms (may be
- * NULL) receives the device time of the copy after tc_kv_migrate_wait. */
+/* KV migration -- replaces transfer_time_ms at engine.hpp:402 (degrade / backflow) and
+ * engine.hpp:516 (init); cost_model.hpp:81-85.
+ *
+ * tc_kv_migrate_async moves the KV of req_id from src to dst: every page src holds for it (at
+ * least the first n_tokens rows; a step in flight on src may have written one more row). Pages on
+ * dst are allocated now; the copy kernel runs on src's high-priority copy stream for dst, after
+ * src's in-flight step, and pushes over NVLink when the instances are on different GPUs. The call
+ * never blocks: src's pages return to its pool when the copy completes, and dst's next step that
+ * touches req_id (and any later migration or release of it) orders after the copy on the GPU.
+ * Several migrations may be in flight from and to one instance. The returned event reports
+ * completion and the copy's device time; destroy it when done (the copy is unaffected). */
+typedef struct tc_event tc_event;
+tc_status tc_kv_migrate_async(tc_instance* src, tc_instance* dst, int64_t req_id, int64_t n_tokens, tc_event** ev);
+tc_status tc_event_query(tc_event* ev, int32_t* done);                      /* non-blocking */
+tc_status tc_event_wait(tc_event* ev, float* copy_ms, int64_t* bytes);      /* blocks until the copy is done */
+tc_status tc_event_destroy(tc_event* ev);
+/* Synchronous form (one migration per source at a time): tc_kv_migrate, then tc_kv_migrate_wait
+ * returns the copy's device time and bytes. */
 tc_status tc_kv_migrate(tc_instance* src, tc_instance* dst, int64_t req_id, int64_t n_tokens);
 tc_status tc_kv_migrate_wait(tc_instance* src, float* copy_ms, int64_t* bytes);
+/* Grid of the copy kernel (0 = 2 x SMs, full bandwidth; fewer CTAs leave SMs to the steps). */
+tc_status tc_set_migration_ctas(tc_instance* inst, int32_t ctas);
 
 /* Device pointer of the KV pool and its geometry (tests / tools). */
 tc_status tc_kv_pool_info(tc_instance* inst, void** base, int64_t* page_bytes, int64_t* n_pages);

@@ -13,8 +13,10 @@ Qwen2 decoder:
 
   x = E[token]                                  (fp32 residual stream)
   per layer:  h = bf16(RMSNorm(x) * w_attn)
-              qkv = bf16(h @ Wqkv^T [+ b])      q|k|v rows, fp32 accumulate
-              q, k = bf16(RoPE(q, k))           half-split rotation, theta, fp64 table
+              qkv = h @ Wqkv^T [+ b]            q|k|v rows, fp32 accumulate (no rounding yet)
+              q, k = bf16(RoPE(q, k)), v = bf16(v)   half-split rotation, theta, fp64 table;
+                                                ONE bf16 rounding after RoPE, as the fused
+                                                QKV epilogue stores it (gemm_ws.cuh)
               o = bf16(softmax(q k^T / sqrt(dh), causal, GQA h -> h // G) v)
               x += o @ Wo^T
               h = bf16(RMSNorm(x) * w_mlp)
@@ -199,10 +201,14 @@ def apply_rope(x: torch.Tensor, pos: torch.Tensor, cos: torch.Tensor, sin: torch
 class RefModel:
     """Per-request incremental decoder with a dense KV cache (the token oracle)."""
 
-    def __init__(self, dims: Dims, weights: dict, max_pos: int = 4096):
+    def __init__(self, dims: Dims, weights: dict, max_pos: int = 4096, round_bf16: bool = True):
+        """round_bf16=False drops every bf16 storage point (pure fp32 math): the mode in which the
+        restatement is pinned against an independent Llama / Qwen2 implementation
+        (tests/test_oracle_model_pinning.py: HF transformers, tests/golden/hf_*.npz)."""
         self.m = dims
         self.w = weights
         self.cos, self.sin = rope_table(dims, max_pos)
+        self.rnd = bf16 if round_bf16 else (lambda t: t)
 
     def new_cache(self):
         return [{"k": None, "v": None} for _ in range(self.m.n_layers)]
@@ -210,7 +216,7 @@ class RefModel:
     @torch.no_grad()
     def forward(self, tokens, pos0: int, cache) -> torch.Tensor:
         """Feed tokens at positions pos0.. ; returns final hidden (fp32) [T, d]."""
-        m, w = self.m, self.w
+        m, w, bf16 = self.m, self.w, self.rnd
         H, Hk, dh = m.n_heads, m.n_kv_heads, m.head_dim
         G = H // Hk
         toks = torch.as_tensor(np.asarray(tokens, dtype=np.int64))
@@ -219,10 +225,10 @@ class RefModel:
         x = w["embed"][toks].clone()
         for l, L in enumerate(w["layers"]):
             h = bf16(rmsnorm(x, L["attn_norm"], m.rms_eps))
-            qkv = bf16(h @ L["qkv"].T + L["qkv_bias"])
+            qkv = h @ L["qkv"].T + L["qkv_bias"]
             q = qkv[:, : H * dh].view(T, H, dh)
             k = qkv[:, H * dh:(H + Hk) * dh].view(T, Hk, dh)
-            v = qkv[:, (H + Hk) * dh:].view(T, Hk, dh)
+            v = bf16(qkv[:, (H + Hk) * dh:].view(T, Hk, dh))
             q = bf16(apply_rope(q, pos, self.cos, self.sin))
             k = bf16(apply_rope(k, pos, self.cos, self.sin))
             c = cache[l]
@@ -245,7 +251,7 @@ class RefModel:
 
     @torch.no_grad()
     def logits(self, x_rows: torch.Tensor) -> torch.Tensor:
-        h = bf16(rmsnorm(x_rows, self.w["final_norm"], self.m.rms_eps))
+        h = self.rnd(rmsnorm(x_rows, self.w["final_norm"], self.m.rms_eps))
         return h @ self.w["lm_head"].T
 
     @torch.no_grad()

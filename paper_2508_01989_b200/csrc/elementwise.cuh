@@ -200,4 +200,40 @@ __global__ void __launch_bounds__(512) kv_copy_pages(const uint4* __restrict__ s
   }
 }
 
+// Page lists of one asynchronous migration travel in the kernel's parameter space (16 KB of the
+// 32 KB limit): no staging buffer, no H2D copy on the copy stream, any number of migrations in
+// flight. Requests longer than kMigPagesPerLaunch pages take several launches.
+constexpr int kMigPagesPerLaunch = 2040;
+struct MigPages {
+  int n;
+  int32_t src[kMigPagesPerLaunch];
+  int32_t dst[kMigPagesPerLaunch];
+};
+
+__global__ void __launch_bounds__(512) kv_migrate_pages(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
+                                                        const __grid_constant__ MigPages pl, long long page_vec) {
+  const long long total = (long long)pl.n * page_vec;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total; base += stride * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < total) {
+        const int pg = (int)(i / page_vec);
+        v[u] = ld_nc_v4(src_pool + (long long)pl.src[pg] * page_vec + (i - (long long)pg * page_vec));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < total) {
+        const int pg = (int)(i / page_vec);
+        st_global_v4(dst_pool + (long long)pl.dst[pg] * page_vec + (i - (long long)pg * page_vec), v[u]);
+      }
+    }
+  }
+}
+
 }  // namespace tc

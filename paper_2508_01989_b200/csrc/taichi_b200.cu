@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -465,6 +466,11 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   const int N = (int)w.rows;
   TC_REQUIRE(N % 256 == 0, "gemm_ws: weight rows must be a multiple of 256");
   const int pairs = sms / 2;
+  static const int env_splits = [] {
+    const char* e = std::getenv("TC_WS_SPLITS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_splits == 0 && env_splits > 0) force_splits = env_splits;
   tc::GemmArgs args = plan_gemm_ws(M, N, (int)w.cols, epi, sms, force_splits);
   // off by default: measured -0.5% (mixed) / -1.7% (decode-only) -- the fill is not DRAM-bound
   static const bool l2_next = [] {
@@ -673,7 +679,100 @@ struct PhaseTimer {
   }
 };
 
+// ------------------------------------------------------------------ KV pool
+// A CUDA event shared by everyone who must order against it (a migration's copy-done event is
+// referenced by its tc_event, by the destination's inbound list and by the source pool's quarantine).
+struct SharedEvent {
+  cudaEvent_t e = nullptr;
+  int device = 0;
+  SharedEvent(int dev, bool timing) : device(dev) {
+    DeviceGuard g(dev);
+    TC_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  }
+  ~SharedEvent() {
+    DeviceGuard g(device);
+    if (e) cudaEventDestroy(e);
+  }
+  bool done() const { return cudaEventQuery(e) == cudaSuccess; }
+};
+using EvPtr = std::shared_ptr<SharedEvent>;
+
+// Page-major KV pool of one GPU. Several instances on one GPU may share it (tc_instance_desc.
+// share_kv_pool): one allocator, so co-located instances draw on the whole HBM budget instead of
+// fixed per-instance slices. Pages an in-flight copy still reads (the source side of a migration)
+// or writes (the destination of a migration whose request is released early) sit in quarantine
+// until that copy's event completes; allocation reclaims them, blocking on the oldest only when the
+// free list alone cannot serve the request.
+struct KvPool {
+  int device = 0;
+  __nv_bfloat16* kv = nullptr;
+  int64_t page_elems = 0, n_pages = 0;
+  std::mutex mu;
+  std::vector<int32_t> free_pages;
+  struct Held {
+    EvPtr ev;
+    std::vector<int32_t> pages;
+  };
+  std::deque<Held> quarantine;
+  int64_t quarantined = 0;
+  ~KvPool() {
+    DeviceGuard g(device);
+    if (kv) cudaFree(kv);
+  }
+  // caller holds mu
+  void reclaim(bool block_until, int64_t want) {
+    while (!quarantine.empty()) {
+      Held& h = quarantine.front();
+      if (!h.ev->done()) {
+        if (!block_until || (int64_t)free_pages.size() >= want) break;
+        DeviceGuard g(device);
+        TC_CUDA(cudaEventSynchronize(h.ev->e));
+      }
+      for (auto p = h.pages.rbegin(); p != h.pages.rend(); ++p) free_pages.push_back(*p);
+      quarantined -= (int64_t)h.pages.size();
+      quarantine.pop_front();
+    }
+  }
+  void take(std::vector<int32_t>& t, int64_t need, int64_t req) {
+    std::lock_guard<std::mutex> lk(mu);
+    const int64_t more = need - (int64_t)t.size();
+    if ((int64_t)free_pages.size() < more) reclaim(false, more);
+    if ((int64_t)free_pages.size() < more) reclaim(true, more);
+    if ((int64_t)free_pages.size() < more)
+      throw TcFail{TC_ERR_OOM, "KV pool exhausted (req " + std::to_string(req) + ", need " + std::to_string(more) +
+                                   " more pages, free " + std::to_string(free_pages.size()) + " of " +
+                                   std::to_string(n_pages) + ")"};
+    while ((int64_t)t.size() < need) {
+      t.push_back(free_pages.back());
+      free_pages.pop_back();
+    }
+  }
+  void give(std::vector<int32_t>&& pages, const EvPtr& busy_until) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (busy_until && !busy_until->done()) {
+      quarantined += (int64_t)pages.size();
+      quarantine.push_back(Held{busy_until, std::move(pages)});
+      return;
+    }
+    for (auto p = pages.rbegin(); p != pages.rend(); ++p) free_pages.push_back(*p);
+  }
+  int64_t free_count() {
+    std::lock_guard<std::mutex> lk(mu);
+    reclaim(false, 0);
+    return (int64_t)free_pages.size();
+  }
+};
+
 }  // namespace
+
+// An asynchronous KV migration (tc_kv_migrate_async): copy-done event + timing.
+struct tc_event {
+  EvPtr done;                       // copy finished (destination pages valid, source pages reusable)
+  cudaEvent_t t0 = nullptr;         // copy start on the migration stream (timing)
+  int device = 0;
+  int64_t bytes = 0, pages = 0;
+  int32_t peer = 0;                 // 1 if source and destination are on different GPUs
+};
 
 struct tc_instance {
   tc_instance_desc desc{};
@@ -685,14 +784,17 @@ struct tc_instance {
   __nv_bfloat16 *embed = nullptr, *final_norm = nullptr;
   WMat lm_head;
   std::vector<LayerW> layers;
-  // KV pool
-  __nv_bfloat16* kv = nullptr;
+  // KV pool (possibly shared with other instances on this GPU) and this instance's page tables
+  std::shared_ptr<KvPool> pool;
+  __nv_bfloat16* kv = nullptr;  // == pool->kv
   int64_t page_elems = 0, n_pages = 0;
-  std::vector<int32_t> free_pages;
   CUtensorMap kv_map;  // 3-D view {64 dims, pool rows, head_dim/64 halves}; box = one (K, V) page pair
   CUtensorMap kv2_map;  // 2-D view {head_dim, pool rows}; box = one 64-dim half of one K or V block
   CUtensorMap q_map;    // 3-D view of the q heads of the qkv buffer {head_dim, q heads, rows}
   std::unordered_map<int64_t, std::vector<int32_t>> tables;
+  // requests whose pages here are still being written by an inbound migration copy: steps,
+  // outbound copies and releases of the request order after the event
+  std::unordered_map<int64_t, EvPtr> inbound;
   // activations
   int qkv_n = 0;
   float* resid = nullptr;
@@ -723,13 +825,13 @@ struct tc_instance {
   int launches = 0;       // kernels launched by the last step
   int64_t h2d_bytes = 0;  // bytes copied H2D by the last step
 
-  // migration
-  int32_t* mig_host = nullptr;
-  int32_t* mig_dev = nullptr;
-  int mig_cap = 0;
-  cudaEvent_t mig_a = nullptr, mig_b = nullptr;
-  bool mig_pending = false;
-  int64_t mig_bytes = 0;
+  // migration: one high-priority copy stream per destination (copies to different destinations
+  // overlap each other and this instance's steps); tail = this instance's step stream position a
+  // copy must follow (a step in flight may still write the request's newest row)
+  std::unordered_map<const tc_instance*, cudaStream_t> mig_streams;
+  cudaEvent_t mig_tail = nullptr;
+  tc_event* last_mig = nullptr;  // tc_kv_migrate / tc_kv_migrate_wait (synchronous form)
+  int mig_ctas = 0;              // copy kernel grid (0 = 2 x SMs)
   PhaseTimer prof;
 };
 
@@ -898,11 +1000,7 @@ void alloc_buffers(tc_instance* I) {
   TC_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
   TC_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
   TC_CUDA(cudaEventCreate(&I->ev_stop));
-  TC_CUDA(cudaEventCreate(&I->mig_a));
-  TC_CUDA(cudaEventCreate(&I->mig_b));
-  I->mig_cap = (int)(2 * max_pages_per_seq + 16);
-  TC_CUDA(cudaMallocHost(&I->mig_host, (size_t)I->mig_cap * 4));
-  TC_CUDA(cudaMalloc(&I->mig_dev, (size_t)I->mig_cap * 4));
+  TC_CUDA(cudaEventCreateWithFlags(&I->mig_tail, cudaEventDisableTiming));
 }
 
 void ensure_pages(tc_instance* I, int64_t req, int64_t n_tokens) {
@@ -910,19 +1008,27 @@ void ensure_pages(tc_instance* I, int64_t req, int64_t n_tokens) {
   const int64_t need = (n_tokens + ps - 1) / ps;
   std::vector<int32_t>& t = I->tables[req];
   if ((int64_t)t.size() >= need) return;
-  if ((int64_t)I->free_pages.size() < need - (int64_t)t.size())
-    throw TcFail{TC_ERR_OOM, "KV pool exhausted (req " + std::to_string(req) + ", need " + std::to_string(need) +
-                                 " pages, free " + std::to_string(I->free_pages.size()) + ")"};
-  while ((int64_t)t.size() < need) {
-    t.push_back(I->free_pages.back());
-    I->free_pages.pop_back();
-  }
+  I->pool->take(t, need, req);
 }
 
-void release_pages(tc_instance* I, int64_t req) {
+// Inbound copy of req still running? (drops the entry once its event completed)
+EvPtr inbound_pending(tc_instance* I, int64_t req) {
+  auto it = I->inbound.find(req);
+  if (it == I->inbound.end()) return nullptr;
+  if (it->second->done()) {
+    I->inbound.erase(it);
+    return nullptr;
+  }
+  return it->second;
+}
+
+// busy_until: the pages stay quarantined until this event (an outbound copy still reading them)
+void release_pages(tc_instance* I, int64_t req, EvPtr busy_until = nullptr) {
   auto it = I->tables.find(req);
   if (it == I->tables.end()) return;
-  for (auto p = it->second.rbegin(); p != it->second.rend(); ++p) I->free_pages.push_back(*p);
+  if (!busy_until) busy_until = inbound_pending(I, req);  // an inbound copy may still write them
+  I->inbound.erase(req);
+  I->pool->give(std::move(it->second), busy_until);
   I->tables.erase(it);
 }
 
@@ -1018,11 +1124,25 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     T += st->prefill[i].n_tokens;
   }
   TC_REQUIRE(T <= I->desc.max_step_tokens, "step: too many tokens");
-  for (int i = 0; i < n_dec; ++i)
+  for (int i = 0; i < n_dec; ++i) {
     TC_REQUIRE(st->decode[i].pos >= 0 && st->decode[i].pos < I->desc.max_context, "step: bad decode position");
+    TC_REQUIRE(st->decode[i].token_id >= 0 && st->decode[i].token_id < m.vocab, "step: token id out of range");
+  }
+  // every argument is checked before any page is allocated (a rejected step changes nothing)
+  for (int i = 0; i < n_pf; ++i) {
+    TC_REQUIRE(st->prefill[i].token_ids != nullptr, "step: null token ids");
+    for (int k = 0; k < st->prefill[i].n_tokens; ++k)
+      TC_REQUIRE(st->prefill[i].token_ids[k] >= 0 && st->prefill[i].token_ids[k] < m.vocab, "step: token id out of range");
+  }
   // physical pages for every new position
   for (int i = 0; i < n_pf; ++i) ensure_pages(I, st->prefill[i].req_id, st->prefill[i].pos0 + st->prefill[i].n_tokens);
   for (int i = 0; i < n_dec; ++i) ensure_pages(I, st->decode[i].req_id, st->decode[i].pos + 1);
+  // requests whose KV is still arriving from another instance: the step orders after the copy
+  std::vector<EvPtr> waits;
+  for (int i = 0; i < n_pf; ++i)
+    if (EvPtr e = inbound_pending(I, st->prefill[i].req_id)) waits.push_back(e);
+  for (int i = 0; i < n_dec; ++i)
+    if (EvPtr e = inbound_pending(I, st->decode[i].req_id)) waits.push_back(e);
 
   const int G = m.n_heads / m.n_kv_heads;
 #if TC_PREFILL_MMA_SYNC
@@ -1110,9 +1230,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     const int np = (sl.pos0 + sl.n_tokens + ps - 1) / ps;
     for (int k = 0; k < np; ++k) h[o_bt + bt++] = pages[k];
     for (int k = 0; k < sl.n_tokens; ++k) {
-      const int32_t tok = sl.token_ids[k];
-      TC_REQUIRE(tok >= 0 && tok < m.vocab, "step: token id out of range");
-      h[o_tok + row + k] = tok;
+      h[o_tok + row + k] = sl.token_ids[k];
       h[o_pos + row + k] = sl.pos0 + k;
       h[o_rseq + row + k] = i;
       h[o_kvrow + row + k] = pages[(sl.pos0 + k) / ps] * ps + (sl.pos0 + k) % ps;
@@ -1146,7 +1264,6 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     const tc_decode_item& di = st->decode[j];
     const int s = n_pf + j;
     const std::vector<int32_t>& pages = I->tables[di.req_id];
-    TC_REQUIRE(di.token_id >= 0 && di.token_id < m.vocab, "step: token id out of range");
     h[o_qs + s] = row;
     h[o_ql + s] = 1;
     h[o_p0 + s] = di.pos;
@@ -1214,6 +1331,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   if (I->prof.on) I->prof.reset();
   I->launches = 0;
   I->h2d_bytes = (int64_t)off * 4;
+  for (const EvPtr& e : waits) TC_CUDA(cudaStreamWaitEvent(s, e->e, 0));
   TC_CUDA(cudaEventRecord(I->ev_start, s));
   TC_CUDA(cudaMemcpyAsync(I->meta_dev, h, off * 4, cudaMemcpyHostToDevice, s));
   const int32_t* dm = I->meta_dev;
@@ -1375,22 +1493,36 @@ void step_wait(tc_instance* I, tc_step_result* r) {
   float ms = 0.f;
   TC_CUDA(cudaEventElapsedTime(&ms, I->ev_start, I->ev_stop));
   r->gpu_ms = ms;
+  r->attn_pf_sms = I->pf_sms;
 }
+
+void event_destroy(tc_event* ev);
 
 void destroy(tc_instance* I) {
   DeviceGuard dg(I->desc.device);
   if (I->stream) cudaStreamSynchronize(I->stream);
+  for (auto& kv : I->mig_streams) {
+    cudaStreamSynchronize(kv.second);
+    cudaStreamDestroy(kv.second);
+  }
+  if (I->last_mig) event_destroy(I->last_mig);
+  // pages go back to the (possibly shared) pool; copies into them have finished (streams synced
+  // above for outbound; inbound copies are ordered by their events in the pool's quarantine)
+  if (I->pool) {
+    std::vector<int64_t> reqs;
+    for (auto& t : I->tables) reqs.push_back(t.first);
+    for (int64_t r : reqs) release_pages(I, r);
+  }
   auto f = [](void* p) {
     if (p) cudaFree(p);
   };
   I->weight_owner.reset();
-  f(I->kv); f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
+  I->pool.reset();
+  f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
   f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->stream_scr); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
-  f(I->mig_dev);
   if (I->ids_host) cudaFreeHost(I->ids_host);
   if (I->meta_host) cudaFreeHost(I->meta_host);
-  if (I->mig_host) cudaFreeHost(I->mig_host);
-  for (cudaEvent_t e : {I->ev_start, I->ev_stop, I->mig_a, I->mig_b, I->ev_fork, I->ev_join})
+  for (cudaEvent_t e : {I->ev_start, I->ev_stop, I->mig_tail, I->ev_fork, I->ev_join})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : I->prof.pool) cudaEventDestroy(e);
   if (I->stream) cudaStreamDestroy(I->stream);
@@ -1414,47 +1546,88 @@ void enable_peer(int a, int b) {
   done.insert({a, b});
 }
 
-void migrate(tc_instance* src, tc_instance* dst, int64_t req, int64_t n_tokens) {
+// Asynchronous KV migration (K11): every page src holds for req (at least the first n_tokens rows;
+// a step in flight on src may have written one more row, which must travel too -- a request that
+// flows away and back within that step brings it home, engine.hpp:461-493) is pushed into freshly
+// allocated pages of dst by kv_migrate_pages on src's high-priority copy stream for dst, after
+// src's in-flight step. Nothing blocks the host: src's pages return to its pool once the copy's
+// event completes (quarantine), and dst's next step / outbound copy / release of req orders
+// after that event. Across GPUs the kernel's stores go over NVLink (peer access, UVA).
+tc_event* migrate_async(tc_instance* src, tc_instance* dst, int64_t req, int64_t n_tokens) {
   TC_REQUIRE(src && dst && src != dst, "migrate: need two distinct instances");
   TC_REQUIRE(src->page_elems == dst->page_elems && src->desc.page_size == dst->desc.page_size,
              "migrate: instances differ in KV geometry");
-  TC_REQUIRE(!src->mig_pending, "migrate: previous migration on this source not waited");
   auto it = src->tables.find(req);
   TC_REQUIRE(it != src->tables.end(), "migrate: request has no KV on source");
   TC_REQUIRE(dst->tables.find(req) == dst->tables.end() || dst->tables[req].empty(),
              "migrate: request already has KV on destination");
   const int ps = src->desc.page_size;
-  // Every page the source holds moves (at least the n_tokens rows asked for): a step still in
-  // flight on the source may have written the next row into a page beyond n_tokens, and a request
-  // that flows away and back within that step must bring that row home (engine.hpp:461-493
-  // commits the step's token if the request is resident again when the step completes).
-  TC_REQUIRE((n_tokens + ps - 1) / ps <= (int64_t)it->second.size(), "migrate: source holds fewer pages than requested");
+  TC_REQUIRE(n_tokens >= 0 && (n_tokens + ps - 1) / ps <= (int64_t)it->second.size(),
+             "migrate: source holds fewer pages than requested");
   const int64_t np = (int64_t)it->second.size();
-  TC_REQUIRE(2 * np <= src->mig_cap, "migrate: request too long");
   ensure_pages(dst, req, np * ps);
-  const std::vector<int32_t>& dp = dst->tables[req];
-  for (int64_t i = 0; i < np; ++i) {
-    src->mig_host[i] = it->second[i];
-    src->mig_host[np + i] = dp[i];
-  }
   enable_peer(src->desc.device, dst->desc.device);
-  DeviceGuard dg(src->desc.device);
-  cudaStream_t s = src->stream;
-  TC_CUDA(cudaMemcpyAsync(src->mig_dev, src->mig_host, (size_t)2 * np * 4, cudaMemcpyHostToDevice, s));
-  TC_CUDA(cudaEventRecord(src->mig_a, s));
-  const int64_t page_vec = src->page_elems * 2 / 16;
-  const int blocks = (int)std::min<int64_t>(2 * src->sms, std::max<int64_t>(1, np * page_vec / (512 * 4)));
-  if (np > 0)
-    tc::kv_copy_pages<<<blocks, 512, 0, s>>>(reinterpret_cast<const uint4*>(src->kv), reinterpret_cast<uint4*>(dst->kv),
-                                             src->mig_dev, src->mig_dev + np, (int)np, page_vec);
-  TC_CUDA(cudaGetLastError());
-  TC_CUDA(cudaEventRecord(src->mig_b, s));
-  // destination's next step must see the copied pages
-  TC_CUDA(cudaStreamWaitEvent(dst->stream, src->mig_b, 0));
-  // pages become reusable on the source once the copy is ordered on its stream
-  release_pages(src, req);
-  src->mig_pending = true;
-  src->mig_bytes = np * src->page_elems * 2;
+  std::unique_ptr<tc_event> ev(new tc_event());
+  ev->device = src->desc.device;
+  ev->pages = np;
+  ev->bytes = np * src->page_elems * 2;
+  ev->peer = src->desc.device != dst->desc.device;
+  ev->done = std::make_shared<SharedEvent>(src->desc.device, true);
+  {
+    DeviceGuard dg(src->desc.device);
+    TC_CUDA(cudaEventCreate(&ev->t0));
+    cudaStream_t& cs = src->mig_streams[dst];
+    if (!cs) {
+      int lo = 0, hi = 0;
+      TC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      TC_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
+    }
+    // after src's in-flight step (it may write the newest row) and after any inbound copy of req
+    TC_CUDA(cudaEventRecord(src->mig_tail, src->stream));
+    TC_CUDA(cudaStreamWaitEvent(cs, src->mig_tail, 0));
+    if (EvPtr in = inbound_pending(src, req)) TC_CUDA(cudaStreamWaitEvent(cs, in->e, 0));
+    // dst pages may be quarantined pages of an earlier copy: reclaim only hands them out once
+    // their event completed, so no ordering is needed on the destination side
+    TC_CUDA(cudaEventRecord(ev->t0, cs));
+    const std::vector<int32_t>& sp = it->second;
+    const std::vector<int32_t>& dp = dst->tables[req];
+    const int64_t page_vec = src->page_elems * 2 / 16;
+    const int cap = src->mig_ctas > 0 ? src->mig_ctas : 2 * src->sms;
+    for (int64_t b0 = 0; b0 < np; b0 += tc::kMigPagesPerLaunch) {
+      tc::MigPages pl;
+      pl.n = (int)std::min<int64_t>(tc::kMigPagesPerLaunch, np - b0);
+      for (int i = 0; i < pl.n; ++i) {
+        pl.src[i] = sp[b0 + i];
+        pl.dst[i] = dp[b0 + i];
+      }
+      const int blocks = (int)std::min<int64_t>(cap, std::max<int64_t>(1, pl.n * page_vec / (512 * 4)));
+      tc::kv_migrate_pages<<<blocks, 512, 0, cs>>>(reinterpret_cast<const uint4*>(src->kv),
+                                                   reinterpret_cast<uint4*>(dst->kv), pl, page_vec);
+      TC_CUDA(cudaGetLastError());
+    }
+    TC_CUDA(cudaEventRecord(ev->done->e, cs));
+  }
+  dst->inbound[req] = ev->done;
+  // source pages return to the pool once the copy has read them
+  release_pages(src, req, ev->done);
+  return ev.release();
+}
+
+void event_wait(tc_event* ev, float* copy_ms, int64_t* bytes) {
+  TC_REQUIRE(ev, "event: null");
+  DeviceGuard dg(ev->device);
+  TC_CUDA(cudaEventSynchronize(ev->done->e));
+  float ms = 0.f;
+  TC_CUDA(cudaEventElapsedTime(&ms, ev->t0, ev->done->e));
+  if (copy_ms) *copy_ms = ms;
+  if (bytes) *bytes = ev->bytes;
+}
+
+void event_destroy(tc_event* ev) {
+  if (!ev) return;
+  DeviceGuard dg(ev->device);
+  if (ev->t0) cudaEventDestroy(ev->t0);
+  delete ev;
 }
 
 }  // namespace
@@ -1492,7 +1665,7 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     check_dims(desc->dims);
     TC_REQUIRE(desc->page_size == 16, "create: page_size must be 16");
     TC_REQUIRE(desc->max_step_tokens >= 1 && desc->max_seqs >= 1 && desc->max_context >= 16, "create: bad limits");
-    TC_REQUIRE(desc->kv_pool_tokens >= desc->page_size, "create: KV pool too small");
+    TC_REQUIRE(desc->kv_pool_tokens <= 0 || desc->kv_pool_tokens >= desc->page_size, "create: KV pool too small");
     I = new tc_instance();
     I->desc = *desc;
     I->d = desc->dims;
@@ -1525,9 +1698,32 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
     alloc_buffers(I);
     const tc_model_dims& m = I->d;
     I->page_elems = (int64_t)m.n_layers * 2 * m.n_kv_heads * desc->page_size * m.head_dim;
-    I->n_pages = (desc->kv_pool_tokens + desc->page_size - 1) / desc->page_size;
-    TC_CUDA(cudaMalloc(&I->kv, (size_t)I->n_pages * I->page_elems * 2));
-    TC_CUDA(cudaMemsetAsync(I->kv, 0, (size_t)I->n_pages * I->page_elems * 2, I->stream));
+    if (desc->share_kv_pool) {
+      const tc_instance* o = desc->share_kv_pool;
+      TC_REQUIRE(o->desc.device == desc->device && o->page_elems == I->page_elems,
+                 "create: share_kv_pool needs the same device and KV geometry");
+      I->pool = o->pool;
+    } else {
+      I->pool = std::make_shared<KvPool>();
+      I->pool->device = desc->device;
+      I->pool->page_elems = I->page_elems;
+      int64_t tokens = desc->kv_pool_tokens;
+      if (tokens <= 0) {
+        // auto: every free byte of HBM but a 4 GiB reserve (production sizing)
+        size_t free_b = 0, total_b = 0;
+        TC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const int64_t usable = (int64_t)free_b - ((int64_t)4 << 30);
+        TC_REQUIRE(usable > I->page_elems * 2, "create: no HBM left for a KV pool");
+        tokens = usable / (I->page_elems * 2) * desc->page_size;
+      }
+      I->pool->n_pages = (tokens + desc->page_size - 1) / desc->page_size;
+      TC_CUDA(cudaMalloc(&I->pool->kv, (size_t)I->pool->n_pages * I->page_elems * 2));
+      TC_CUDA(cudaMemsetAsync(I->pool->kv, 0, (size_t)I->pool->n_pages * I->page_elems * 2, I->stream));
+      I->pool->free_pages.resize(I->pool->n_pages);
+      for (int64_t i = 0; i < I->pool->n_pages; ++i) I->pool->free_pages[i] = (int32_t)(I->pool->n_pages - 1 - i);  // pop_back -> 0,1,..
+    }
+    I->kv = I->pool->kv;
+    I->n_pages = I->pool->n_pages;
     {
       const uint64_t rows = (uint64_t)I->n_pages * m.n_layers * 2 * m.n_kv_heads * desc->page_size;
       TC_REQUIRE(rows < (1ull << 31), "create: KV pool too large for 32-bit TMA row coordinates");
@@ -1550,8 +1746,6 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
       const cuuint32_t box[2] = {64, (cuuint32_t)desc->page_size};
       I->kv2_map = encode_map(I->kv, 2, dims, strides, box);
     }
-    I->free_pages.resize(I->n_pages);
-    for (int64_t i = 0; i < I->n_pages; ++i) I->free_pages[i] = (int32_t)(I->n_pages - 1 - i);  // pop_back -> 0,1,..
     TC_CUDA(cudaStreamSynchronize(I->stream));
   });
   if (st != TC_OK) {
@@ -1601,24 +1795,56 @@ tc_status tc_kv_stats(tc_instance* inst, int64_t req_id, int64_t* req_pages, int
     TC_REQUIRE(inst, "stats: null instance");
     auto it = inst->tables.find(req_id);
     if (req_pages) *req_pages = it == inst->tables.end() ? 0 : (int64_t)it->second.size();
-    if (free_pages) *free_pages = (int64_t)inst->free_pages.size();
+    if (free_pages) *free_pages = inst->pool->free_count();
   });
 }
 
+tc_status tc_kv_migrate_async(tc_instance* src, tc_instance* dst, int64_t req_id, int64_t n_tokens, tc_event** ev) {
+  return guarded([&] {
+    TC_REQUIRE(ev, "migrate_async: null event out-pointer");
+    *ev = migrate_async(src, dst, req_id, n_tokens);
+  });
+}
+
+tc_status tc_event_query(tc_event* ev, int32_t* done) {
+  return guarded([&] {
+    TC_REQUIRE(ev && done, "event_query: null argument");
+    const cudaError_t e = cudaEventQuery(ev->done->e);
+    if (e != cudaSuccess && e != cudaErrorNotReady) TC_CUDA(e);
+    *done = e == cudaSuccess;
+  });
+}
+
+tc_status tc_event_wait(tc_event* ev, float* copy_ms, int64_t* bytes) {
+  return guarded([&] { event_wait(ev, copy_ms, bytes); });
+}
+
+tc_status tc_event_destroy(tc_event* ev) {
+  return guarded([&] { event_destroy(ev); });
+}
+
 tc_status tc_kv_migrate(tc_instance* src, tc_instance* dst, int64_t req_id, int64_t n_tokens) {
-  return guarded([&] { migrate(src, dst, req_id, n_tokens); });
+  return guarded([&] {
+    TC_REQUIRE(src, "migrate: null source");
+    TC_REQUIRE(!src->last_mig, "migrate: previous migration on this source not waited");
+    src->last_mig = migrate_async(src, dst, req_id, n_tokens);
+  });
 }
 
 tc_status tc_kv_migrate_wait(tc_instance* src, float* copy_ms, int64_t* bytes) {
   return guarded([&] {
-    TC_REQUIRE(src && src->mig_pending, "migrate_wait: no migration in flight");
-    DeviceGuard dg(src->desc.device);
-    TC_CUDA(cudaEventSynchronize(src->mig_b));
-    float ms = 0.f;
-    TC_CUDA(cudaEventElapsedTime(&ms, src->mig_a, src->mig_b));
-    if (copy_ms) *copy_ms = ms;
-    if (bytes) *bytes = src->mig_bytes;
-    src->mig_pending = false;
+    TC_REQUIRE(src && src->last_mig, "migrate_wait: no migration in flight");
+    tc_event* ev = src->last_mig;
+    src->last_mig = nullptr;
+    std::unique_ptr<tc_event, void (*)(tc_event*)> hold(ev, event_destroy);
+    event_wait(ev, copy_ms, bytes);
+  });
+}
+
+tc_status tc_set_migration_ctas(tc_instance* inst, int32_t ctas) {
+  return guarded([&] {
+    TC_REQUIRE(inst && ctas >= 0, "migration_ctas: bad argument");
+    inst->mig_ctas = ctas;
   });
 }
 

@@ -64,7 +64,7 @@ class _StepDesc(C.Structure):
 class _StepResult(C.Structure):
     _fields_ = [("n_sampled", C.c_int32), ("sampled_ids", C.POINTER(C.c_int32)),
                 ("logits", C.POINTER(C.c_float)), ("gpu_ms", C.c_float), ("launches", C.c_int32),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("attn_pf_sms", C.c_int32)]
 
 
 _lib: Optional[C.CDLL] = None
@@ -130,6 +130,7 @@ class StepOutput:
     launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    attn_pf_sms: int = 0          # SMs prefill attention ran on beside decode attention (0 = serial)
 
 
 class Instance:
@@ -198,11 +199,11 @@ class Instance:
         ids = np.zeros(max(1, n), dtype=np.int32)
         logits = np.zeros((max(1, n), self.dims.vocab), dtype=np.float32) if self._pending_keep else None
         res = _StepResult(0, ids.ctypes.data_as(C.POINTER(C.c_int32)),
-                          logits.ctypes.data_as(C.POINTER(C.c_float)) if logits is not None else None, 0.0, 0, 0, 0)
+                          logits.ctypes.data_as(C.POINTER(C.c_float)) if logits is not None else None, 0.0, 0, 0, 0, 0)
         _check(lib.tc_step_wait(self._h, C.byref(res)))
         return StepOutput(ids[:res.n_sampled].copy(),
                           logits[:res.n_sampled].copy() if logits is not None else None, float(res.gpu_ms),
-                          int(res.launches), int(res.h2d_bytes), int(res.d2h_bytes))
+                          int(res.launches), int(res.h2d_bytes), int(res.d2h_bytes), int(res.attn_pf_sms))
 
     def step(self, prefill=(), decode=(), keep_logits=False) -> StepOutput:
         self.launch(prefill, decode, keep_logits)

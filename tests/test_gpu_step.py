@@ -1,12 +1,15 @@
 """The hybrid step through the C ABI (tc_step_launch / tc_step_wait) vs the CPU oracle
-(oracle/model_ref.py, parity UNPINNED -- see its header).
+(oracle/model_ref.py; its fp32 mode is pinned to HF transformers by test_oracle_model_pinning.py).
 
-Stated tolerances:
-  * logits: max |gpu - oracle| <= 0.05 * std(oracle logits) + 0.02 (bf16 storage points are
-    emulated by the oracle; remaining differences are fp32 accumulation order, bf16 rounding
-    of attention probabilities, exp2 approximations);
-  * greedy tokens: identical except at near-ties, where the oracle's top-2 gap < 0.02; after a
-    near-tie divergence the oracle continues from the GPU token (teacher forcing).
+Stated tolerances (from the measured budget of tools/parity_budget.py,
+profiles/r02/parity_budget_*.json):
+  * logits: max |gpu - oracle| <= LOGIT_REL * std(oracle logits) + LOGIT_ABS. The oracle emulates
+    every bf16 storage point of the GPU path; what remains is fp32 accumulation order (split-K
+    partials are reduced in arrival order), bf16 rounding of the unnormalised attention
+    probabilities against a running max, and exp2 approximations.
+  * greedy tokens: a GPU token g may differ from the oracle's token r only where that is
+    consistent with the logit bound, i.e. oracle[r] - oracle[g] <= 2 * logit_tol; the oracle then
+    continues from the GPU token (teacher forcing). Logits are checked on every sampled row.
 """
 import numpy as np
 import pytest
@@ -16,21 +19,30 @@ from oracle import model_ref as mr
 
 pytestmark = pytest.mark.gpu
 
-NEAR_TIE = 0.02
+LOGIT_REL, LOGIT_ABS = 0.08, 0.01
 
 
 def logit_tol(ref):
-    return 0.05 * float(ref.std()) + 0.02
+    return LOGIT_REL * float(ref.std()) + LOGIT_ABS
 
 
-def check_logits(gpu, ref):
-    gpu = torch.as_tensor(gpu)
+def check_row(gpu_token, gpu_logits, ref):
+    """Returns True when the tokens differ (an allowed near-tie)."""
+    tol = logit_tol(ref)
+    gpu = torch.as_tensor(gpu_logits)
     err = (gpu - ref).abs().max().item()
-    assert err <= logit_tol(ref), f"max |dlogit| {err:.4f} > {logit_tol(ref):.4f}"
+    assert err <= tol, f"max |dlogit| {err:.4f} > {tol:.4f}"
+    assert int(torch.argmax(gpu)) == gpu_token, "sampled id is not the argmax of the returned logits"
+    ref_tok = int(torch.argmax(ref))
+    if ref_tok == gpu_token:
+        return False
+    gap = float(ref[ref_tok] - ref[gpu_token])
+    assert gap <= 2 * tol, f"token mismatch {gpu_token} vs {ref_tok}: oracle gap {gap:.4f} > 2 x tol {tol:.4f}"
+    return True
 
 
 class Follower:
-    """Oracle decoder for one request, teacher-forced on GPU tokens at near-ties."""
+    """Oracle decoder for one request, teacher-forced on GPU tokens."""
 
     def __init__(self, model, prompt):
         self.model, self.cache, self.pos = model, model.new_cache(), 0
@@ -42,15 +54,11 @@ class Follower:
         self.x = self.model.forward(list(toks), self.pos, self.cache)
         self.pos += len(toks)
 
-    def check(self, gpu_token, gpu_logits=None):
-        lg = self.model.logits(self.x[-1:])[0]
-        if gpu_logits is not None:
-            check_logits(gpu_logits, lg)
-        top2 = torch.topk(lg, 2).values
-        ref_tok = int(torch.argmax(lg))
-        if ref_tok != gpu_token:
-            assert float(top2[0] - top2[1]) < NEAR_TIE, f"token mismatch {gpu_token} vs {ref_tok} (not a near-tie)"
-            self.near_ties += 1
+    def ref_logits(self):
+        return self.model.logits(self.x[-1:])[0]
+
+    def check(self, gpu_token, gpu_logits):
+        self.near_ties += check_row(gpu_token, gpu_logits, self.ref_logits())
 
 
 @pytest.fixture(scope="module")
@@ -146,9 +154,9 @@ def test_tiny_decode_page_stream_splits(tiny, lengths):
         rid = 200 + k
         prompt = mr.prompt_tokens(11, rid, n, 1024)
         for s0 in range(0, n, 2048):
-            out = inst.step(prefill=[(rid, s0, prompt[s0:s0 + 2048], s0 + 2048 >= n)])
+            out = inst.step(prefill=[(rid, s0, prompt[s0:s0 + 2048], s0 + 2048 >= n)], keep_logits=True)
         reqs[rid] = [Follower(model, prompt), int(out.sampled[0]), n]
-        reqs[rid][0].check(reqs[rid][1])
+        reqs[rid][0].check(reqs[rid][1], out.logits[0])
     for _ in range(2):
         dec = [(rid, r[2], r[1]) for rid, r in reqs.items()]
         o = inst.step(decode=dec, keep_logits=True)
@@ -189,7 +197,7 @@ def test_tiny_migration_between_instances(tiny):
     dst = Instance("tiny", weight_seed=11, kv_pool_tokens=1 << 14, max_step_tokens=512, max_seqs=16, max_context=4096)
     rid = 77
     prompt = mr.prompt_tokens(11, rid, 150, 1024)
-    out = src.step(prefill=[(rid, 0, prompt, True)])
+    out = src.step(prefill=[(rid, 0, prompt, True)], keep_logits=True)
     src_pages = src.kv_pages(rid)
     before = src.read_pages(src_pages)
     src.migrate_to(dst, rid, len(prompt))
@@ -199,7 +207,7 @@ def test_tiny_migration_between_instances(tiny):
     assert len(dst_pages) == len(src_pages) and nbytes == len(src_pages) * before.shape[1]
     np.testing.assert_array_equal(dst.read_pages(dst_pages), before)
     f = Follower(model, prompt)
-    f.check(int(out.sampled[0]))
+    f.check(int(out.sampled[0]), out.logits[0])
     tok, pos = int(out.sampled[0]), len(prompt)
     for _ in range(6):
         f.feed([tok])
@@ -219,18 +227,18 @@ def test_migration_round_trip_during_inflight_step(tiny):
     dst = Instance("tiny", weight_seed=11, kv_pool_tokens=1 << 14, max_step_tokens=512, max_seqs=16, max_context=4096)
     rid = 78
     prompt = mr.prompt_tokens(11, rid, 32, 1024)  # footprint 33: the next row (32) opens page 3
-    out = src.step(prefill=[(rid, 0, prompt, True)])
+    out = src.step(prefill=[(rid, 0, prompt, True)], keep_logits=True)
     f = Follower(model, prompt)
-    f.check(int(out.sampled[0]))
+    f.check(int(out.sampled[0]), out.logits[0])
     tok, pos = int(out.sampled[0]), len(prompt)
-    src.launch(decode=[(rid, pos, tok)])       # writes row 32, not yet waited
+    src.launch(decode=[(rid, pos, tok)], keep_logits=True)  # writes row 32, not yet waited
     src.migrate_to(dst, rid, pos)              # degrade: footprint - 1 rows requested
     src.migrate_wait()
     dst.migrate_to(src, rid, pos)              # backflow before the step completes
     dst.migrate_wait()
     o = src.wait()
     f.feed([tok])
-    f.check(int(o.sampled[0]))
+    f.check(int(o.sampled[0]), o.logits[0])
     tok, pos = int(o.sampled[0]), pos + 1
     for _ in range(4):
         f.feed([tok])
@@ -277,10 +285,10 @@ def test_llama_shape_mixed_step(llama_l2):
     follow = {}
     toks = {}
     for rid, p in prompts.items():
-        o = inst.step(prefill=[(rid, 0, p, True)])
+        o = inst.step(prefill=[(rid, 0, p, True)], keep_logits=True)
         toks[rid] = int(o.sampled[0])
         follow[rid] = Follower(model, p)
-        follow[rid].check(toks[rid])
+        follow[rid].check(toks[rid], o.logits[0])
     a = mr.prompt_tokens(3, 500, 70, 128256)
     b = mr.prompt_tokens(3, 501, 60, 128256)
     decode = [(rid, len(p), toks[rid]) for rid, p in prompts.items()]
