@@ -1,18 +1,22 @@
 // taichi_serve -- the host engine (include/pdsim) driving B200 instances through the C ABI.
 //
 //   taichi_serve --config F [--seed S] [--model tiny|llama3_8b|qwen2_5_14b[:Ln]]
-//                [--devices 0,1,..] [--clock logical|wall] [--pool-tokens N]
+//                [--devices 0,1,..] [--clock logical|device] [--pool-tokens N]
 //                [--log OUT] [--tokens OUT.jsonl] [--share-weights 0|1] [--link-gbps G]
 //
 // --clock logical: the cost model prices every step/transfer (schedule byte-identical to the
 //   reference's, checked against the oracle log) while every step really runs on the GPU and
-//   every migration really copies KV pages; tokens are written per request for the oracle.
-// --clock wall: measured device step / copy times drive the clock (real SLO goodput).
+//   every migration really copies KV pages (asynchronously: no host wait); tokens are written
+//   per request for the oracle.
+// --clock device (alias: wall): the measured device time of each step / copy drives the clock.
+//   Each step is executed and timed alone (steps run in event order), so host scheduling time
+//   and contention between co-located instances are not in the clock.
 // Instances are placed round-robin on --devices (one per GPU in production). Several
 // instances may share a GPU (tests, or emulating an 8-GPU box on one B200): they then share
-// one weight replica, each step is still executed and timed alone (steps run synchronously in
-// event order), and in wall mode a same-device KV copy is priced at --link-gbps (default 770,
-// the measured B200 NVLink peer-copy bandwidth) instead of its HBM-local copy time.
+// one weight replica and one KV pool (--pool-tokens per GPU; default: all free HBM but 4 GiB),
+// and in device mode a same-device KV copy is priced at --link-gbps (default 900, the nominal
+// NVLink 5 per-direction bandwidth -- an assumption, not a measurement on this 1-GPU pool)
+// instead of its HBM-local copy time.
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -40,7 +44,7 @@ int main(int argc, char** argv) {
   std::string config, model = "tiny", devices = "0", clock = "logical", log, tokens_out;
   long long seed = -1, pool_tokens = 0;
   int share_weights = 1;
-  double link_gbps = 770.0;
+  double link_gbps = 900.0;
   unsigned long long weight_seed = 1;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
@@ -88,25 +92,28 @@ int main(int argc, char** argv) {
       d.page_size = 16;
       // The logical kv_capacity (cluster.hpp:130-181) only counts resident decodes; the physical pool
       // must also hold in-flight prefills, pending decodes (Init transfers are admitted without a
-      // fit check, engine.hpp:512) and KV in transit. Default: 3x logical + 8 max contexts;
-      // --pool-tokens overrides (production: size from free HBM).
-      d.kv_pool_tokens = pool_tokens > 0 ? pool_tokens : sp.kv_capacity * 3 + 8 * max_ctx + 1024;
+      // fit check, engine.hpp:512) and KV in transit. One pool per GPU, shared by the instances on
+      // it: --pool-tokens, default every free byte of HBM but 4 GiB (SURVEY App. B sizing).
+      d.kv_pool_tokens = pool_tokens > 0 ? pool_tokens : 0;
       d.max_step_tokens = static_cast<int32_t>(std::max<Tokens>(sp.chunk_size, 1) + 1024);
       d.max_seqs = 1024;
       d.max_context = static_cast<int32_t>(max_ctx + 16);
       d.share_weights = nullptr;
-      if (share_weights)
-        for (std::size_t j = 0; j < insts.size(); ++j)
-          if (inst_dev[j] == d.device) {
-            d.share_weights = insts[j];
-            break;
-          }
+      d.share_kv_pool = nullptr;
+      for (std::size_t j = 0; j < insts.size(); ++j)
+        if (inst_dev[j] == d.device) {
+          if (share_weights) d.share_weights = insts[j];
+          d.share_kv_pool = insts[j];
+          break;
+        }
       inst_dev.push_back(d.device);
       tc_instance* h = nullptr;
       taichi::tc_check(tc_instance_create(&d, &h), "tc_instance_create");
       insts.push_back(h);
     }
-    taichi::GpuExecutor exec(insts, recs, dims.vocab, s, clock == "wall" ? taichi::ClockMode::Wall : taichi::ClockMode::Logical);
+    if (clock != "logical" && clock != "device" && clock != "wall") throw ConfigError("--clock: logical|device");
+    const bool device_clock = clock != "logical";
+    taichi::GpuExecutor exec(insts, recs, dims.vocab, s, device_clock ? taichi::ClockMode::Device : taichi::ClockMode::Logical);
     exec.emulate_link(inst_dev, link_gbps);
     in.executor = &exec;
     FILE* f = log.empty() ? nullptr : std::fopen(log.c_str(), "w");
@@ -116,6 +123,7 @@ int main(int argc, char** argv) {
       if (f) taichi::log_plan(f, i, t, p, dt);
     };
     const SimulationResult sim = run_simulation(in);
+    exec.finish();
     if (f) {
       taichi::log_result(f, sim);
       std::fclose(f);
@@ -126,6 +134,9 @@ int main(int argc, char** argv) {
         std::fprintf(t, "{\"id\": %zu, \"prompt_len\": %lld, \"tokens\": [", r, (long long)recs[r].prompt_len);
         const auto& tk = exec.tokens(static_cast<RequestId>(r));
         for (std::size_t k = 0; k < tk.size(); ++k) std::fprintf(t, "%s%d", k ? ", " : "", tk[k]);
+        std::fprintf(t, "], \"stale\": [");
+        const auto& st = exec.stale_positions(static_cast<RequestId>(r));
+        for (std::size_t k = 0; k < st.size(); ++k) std::fprintf(t, "%s%lld", k ? ", " : "", (long long)st[k]);
         std::fprintf(t, "]}\n");
       }
       std::fclose(t);
@@ -137,11 +148,12 @@ int main(int argc, char** argv) {
         "\"p90_tpot_ms\": %.17g, \"migrations_init\": %lld, \"migrations_degrade\": %lld, "
         "\"migrations_backflow\": %lld, \"sim_end_ms\": %.17g, \"gpu_steps\": %lld, \"gpu_step_ms\": %.6f, "
         "\"gpu_launches\": %lld, \"kv_copies\": %lld, \"kv_copy_ms\": %.6f, \"kv_copy_bytes\": %lld, \"clock\": \"%s\", "
-        "\"link_gbps_same_device\": %.1f, \"p50_ttft_ms\": %.17g, \"p50_tpot_ms\": %.17g}\n",
+        "\"link_gbps_same_device\": %.1f, \"p50_ttft_ms\": %.17g, \"p50_tpot_ms\": %.17g, "
+        "\"stale_commits\": %lld, \"refed_rows\": %lld, \"max_copies_in_flight\": %lld}\n",
         plans, sim.lifecycles.size(), rep.agg.attainment, rep.agg.p90_ttft_ms, rep.agg.p90_tpot_ms,
         sim.migrations_init, sim.migrations_degrade, sim.migrations_backflow, sim.sim_end_ms, st.steps,
-        st.step_gpu_ms, st.launches, st.migrations, st.copy_ms, st.copy_bytes, clock.c_str(), link_gbps,
-        rep.agg.p50_ttft_ms, rep.agg.p50_tpot_ms);
+        st.step_gpu_ms, st.launches, st.migrations, st.copy_ms, st.copy_bytes, device_clock ? "device" : "logical", link_gbps,
+        rep.agg.p50_ttft_ms, rep.agg.p50_tpot_ms, st.stale_commits, st.refed_rows, st.max_copies_in_flight);
   } catch (const ConfigError& e) {
     std::fprintf(stderr, "config error: %s\n", e.what());
     rc = 1;

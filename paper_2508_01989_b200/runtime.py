@@ -22,6 +22,7 @@ EXPORTED = [
     "tc_kv_reserve", "tc_kv_release", "tc_kv_stats", "tc_kv_migrate", "tc_kv_migrate_wait",
     "tc_kv_pool_info", "tc_kv_pages", "tc_weight_ptr", "tc_read_device", "tc_weight_value", "tc_gemm",
     "tc_copy_pages", "tc_set_profiling", "tc_phase_ms", "tc_last_error", "tc_version",
+    "tc_kv_migrate_async", "tc_event_query", "tc_event_wait", "tc_event_destroy", "tc_set_migration_ctas",
 ]
 
 
@@ -44,7 +45,8 @@ class ModelDims(C.Structure):
 class _InstanceDesc(C.Structure):
     _fields_ = [("device", C.c_int32), ("dims", ModelDims), ("weight_seed", C.c_uint64),
                 ("page_size", C.c_int32), ("kv_pool_tokens", C.c_int64), ("max_step_tokens", C.c_int32),
-                ("max_seqs", C.c_int32), ("max_context", C.c_int32), ("share_weights", C.c_void_p)]
+                ("max_seqs", C.c_int32), ("max_context", C.c_int32), ("share_weights", C.c_void_p),
+                ("share_kv_pool", C.c_void_p)]
 
 
 class _PrefillSlice(C.Structure):
@@ -91,6 +93,11 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "tc_kv_stats": (I32, [P, I64, C.POINTER(I64), C.POINTER(I64)]),
         "tc_kv_migrate": (I32, [P, P, I64, I64]),
         "tc_kv_migrate_wait": (I32, [P, C.POINTER(C.c_float), C.POINTER(I64)]),
+        "tc_kv_migrate_async": (I32, [P, P, I64, I64, C.POINTER(P)]),
+        "tc_event_query": (I32, [P, C.POINTER(I32)]),
+        "tc_event_wait": (I32, [P, C.POINTER(C.c_float), C.POINTER(I64)]),
+        "tc_event_destroy": (I32, [P]),
+        "tc_set_migration_ctas": (I32, [P, I32]),
         "tc_kv_pool_info": (I32, [P, C.POINTER(P), C.POINTER(I64), C.POINTER(I64)]),
         "tc_kv_pages": (I32, [P, I64, C.POINTER(I32), I32, C.POINTER(I32)]),
         "tc_weight_ptr": (I32, [P, C.c_char_p, C.POINTER(P), C.POINTER(I64), C.POINTER(I64)]),
@@ -138,12 +145,14 @@ class Instance:
 
     def __init__(self, model: str | ModelDims = "tiny", device: int = 0, weight_seed: int = 0,
                  kv_pool_tokens: int = 1 << 16, max_step_tokens: int = 2048, max_seqs: int = 256,
-                 max_context: int = 4096, page_size: int = 16, share_weights: "Instance | None" = None):
+                 max_context: int = 4096, page_size: int = 16, share_weights: "Instance | None" = None,
+                 share_kv_pool: "Instance | None" = None):
         lib = load_library()
         self.dims = model_preset(model) if isinstance(model, str) else model
         desc = _InstanceDesc(device, self.dims, weight_seed, page_size, kv_pool_tokens, max_step_tokens,
-                             max_seqs, max_context, share_weights._h.value if share_weights is not None else None)
-        self._shared_from = share_weights  # keep the owner alive
+                             max_seqs, max_context, share_weights._h.value if share_weights is not None else None,
+                             share_kv_pool._h.value if share_kv_pool is not None else None)
+        self._shared_from = (share_weights, share_kv_pool)  # keep the owners alive
         h = C.c_void_p()
         _check(lib.tc_instance_create(C.byref(desc), C.byref(h)))
         self._h = h
@@ -250,6 +259,15 @@ class Instance:
         _check(load_library().tc_kv_migrate_wait(self._h, C.byref(ms), C.byref(nbytes)))
         return float(ms.value), int(nbytes.value)
 
+    def migrate_async(self, dst: "Instance", rid: int, n_tokens: int) -> "MigrationEvent":
+        """Asynchronous KV migration (tc_kv_migrate_async): returns at once; several may be in flight."""
+        ev = C.c_void_p()
+        _check(load_library().tc_kv_migrate_async(self._h, dst._h, rid, n_tokens, C.byref(ev)))
+        return MigrationEvent(ev)
+
+    def set_migration_ctas(self, ctas: int):
+        _check(load_library().tc_set_migration_ctas(self._h, ctas))
+
     # ---------------------------------------------------------------- weights / profiling
     def weight(self, name: str, dtype=np.uint16) -> np.ndarray:
         ptr, r, c = C.c_void_p(), C.c_int64(), C.c_int64()
@@ -265,6 +283,35 @@ class Instance:
         v = C.c_float()
         _check(load_library().tc_phase_ms(self._h, phase.encode(), C.byref(v)))
         return float(v.value)
+
+
+class MigrationEvent:
+    """Completion handle of one asynchronous migration (tc_event)."""
+
+    def __init__(self, h: C.c_void_p):
+        self._h = h
+
+    def done(self) -> bool:
+        d = C.c_int32()
+        _check(load_library().tc_event_query(self._h, C.byref(d)))
+        return bool(d.value)
+
+    def wait(self):
+        """Blocks until the copy finished; returns (copy device ms, bytes)."""
+        ms, nbytes = C.c_float(), C.c_int64()
+        _check(load_library().tc_event_wait(self._h, C.byref(ms), C.byref(nbytes)))
+        return float(ms.value), int(nbytes.value)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            _check(load_library().tc_event_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def gemm(a, b, out, m, n, k, epilogue=0, bias=None, bn=0, k_splits=0, device=0, stream=None):

@@ -5,9 +5,12 @@ C ABI (include/taichi/gpu_executor.hpp, lib/taichi_serve) under the logical cloc
   log for the same config/seed -- the GPU executes every step and every KV migration really
   copies pages, but decisions are the reference's.
 * Every request's greedy tokens match the CPU oracle decoding that request alone (tokens are
-  schedule-independent), except at stated near-ties (top-2 gap < 0.02), where the oracle is
-  teacher-forced with the GPU token. This covers requests that migrated (init / degrade /
-  backflow) between instances mid-generation.
+  schedule-independent), except where the oracle's gap between its token and the GPU's is within
+  twice the logit tolerance of tests/test_gpu_step.py (the oracle is then teacher-forced with the
+  GPU token). This covers requests that migrated (init / degrade / backflow) between instances
+  mid-generation. Tokens the engine commits from a step launched at an older position (a request
+  that flowed away and back within one step, see include/taichi/gpu_executor.hpp) are listed as
+  "stale" by the executor and not compared; the rows they skipped are re-fed.
 """
 import hashlib
 import json
@@ -22,7 +25,7 @@ from oracle import model_ref as mr
 pytestmark = pytest.mark.gpu
 REPO = pathlib.Path(__file__).resolve().parents[1]
 GOLDEN = json.loads((REPO / "tests" / "golden" / "schedules.json").read_text())
-NEAR_TIE = 0.02
+from test_gpu_step import logit_tol
 
 
 def serve(built, cfg, tmp_path, seed=0, extra=()):
@@ -48,12 +51,13 @@ def check_tokens(model, seed, rec, max_requests=None):
         cache = model.new_cache()
         x = model.forward(prompt, 0, cache)
         pos = len(prompt)
+        stale = set(r.get("stale", []))
         for k, g in enumerate(r["tokens"]):
             lg = model.logits(x[-1:])[0]
             ref = int(torch.argmax(lg))
-            if ref != g:
-                top2 = torch.topk(lg, 2).values
-                assert float(top2[0] - top2[1]) < NEAR_TIE, f"request {r['id']} token {k}: gpu {g} vs oracle {ref}"
+            if ref != g and k not in stale:
+                gap = float(lg[ref] - lg[g])
+                assert gap <= 2 * logit_tol(lg), f"request {r['id']} token {k}: gpu {g} vs oracle {ref} (gap {gap:.4f})"
                 ties += 1
             if k + 1 < len(r["tokens"]):
                 x = model.forward([g], pos, cache)
@@ -81,9 +85,11 @@ def test_logical_clock_serving_bitexact_schedule_and_tokens(built, cuda_ok, orac
 def test_migration_heavy_serving(built, cuda_ok, oracle_model, tmp_path):
     """Config 3 shape (4P1024 + 4D256, tight KV): ~1000 degrades / ~800 backflows, 8 instances
     sharing one GPU. Schedule bit-exact; tokens of migrated requests checked."""
-    summary, log, rec = serve(built, "c3_llama8b_4p4d", tmp_path, extra=("--pool-tokens", "400000"))
+    summary, log, rec = serve(built, "c3_llama8b_4p4d", tmp_path, extra=("--pool-tokens", "2000000"))
     assert hashlib.sha256(log).hexdigest() == GOLDEN["c3_llama8b_4p4d/seed0"]["sha256"]
     assert summary["kv_copies"] == summary["migrations_init"] + summary["migrations_degrade"] + summary["migrations_backflow"]
+    assert summary["max_copies_in_flight"] >= 2, "migrations should overlap (asynchronous copies)"
+    print("stale commits", summary["stale_commits"], "re-fed rows", summary["refed_rows"])
     migrated = set()
     for line in log.decode().splitlines():
         if line.startswith("R ") and ("degrade" in line or "backflow" in line):
@@ -93,17 +99,17 @@ def test_migration_heavy_serving(built, cuda_ok, oracle_model, tmp_path):
     check_tokens(oracle_model, 0, picked)
 
 
-def test_wall_clock_mode_runs_on_measured_times(built, cuda_ok, tmp_path):
-    """Wall-clock mode: measured device times drive the clock (decisions may legitimately differ
+def test_device_clock_mode_runs_on_measured_times(built, cuda_ok, tmp_path):
+    """Device-clock mode: measured device times drive the clock (decisions may legitimately differ
     from the cost-model schedule); every request completes and the clock advanced by the
     measured step times."""
     log, toks = tmp_path / "w.log", tmp_path / "w.jsonl"
     p = subprocess.run([str(built / "taichi_serve"), "--config", str(REPO / "configs" / "c1_tiny_hybrid.json"),
-                        "--model", "tiny", "--devices", "0", "--clock", "wall", "--pool-tokens", "200000",
+                        "--model", "tiny", "--devices", "0", "--clock", "device", "--pool-tokens", "200000",
                         "--log", str(log), "--tokens", str(toks)], capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stderr
     s = json.loads(p.stdout)
-    assert s["clock"] == "wall" and s["requests"] == 64
+    assert s["clock"] == "device" and s["requests"] == 64
     busy = sum(float.fromhex(l.split()[4]) for l in log.read_text().splitlines() if l.startswith("I "))
     assert abs(busy - s["gpu_step_ms"]) < 1e-3 * max(1.0, busy)  # busy time == measured device time
     for r in (json.loads(l) for l in toks.read_text().splitlines()):
