@@ -10,11 +10,8 @@
 // (address = half*4096 + row*128 + ((chunk ^ row) & 7) * 16). Completion is tracked with
 // mbarrier transaction counts, so no thread computes per-chunk gather addresses.
 //
-//  * attn_prefill  -- chunked-prefill queries (a chunk may span prompts; each slice
-//    is a sequence) attend causally to the paged prefix + in-chunk keys. CTA =
-//    (16/G tokens x G heads) x 4 consumer warps of one GQA group + 1 TMA producer
-//    warp; 64-key tiles (4 pages) in a 3-stage full/empty mbarrier ring. QK^T and
-//    PV on tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate), online softmax.
+//  * attn_prefill_tc -- chunked-prefill queries attend causally to the paged prefix + in-chunk
+//    keys on tcgen05 (S and O in TMEM), see its section below.
 //  * attn_decode   -- balanced page stream: every SM gets the same number of page-heads
 //    (contiguous range over all (request, kv head) segments); a producer warp streams
 //    K/V pages through a 24-stage TMA ring, 4 consumer warps split the pages and merge
@@ -45,21 +42,7 @@ struct AttnParams {
   float* ws_o;               // [slot][G][DH] partial o of segments cut by CTA boundaries
   float* ws_ml;              // [slot][G][2]
   int* dec_cnt;              // [seg] arrival counters (zero; the last arriver resets)
-  int pf_poly;               // prefill softmax: share of exp2 on the FMA pipe (0 none, 1 = 1/4, 2 = 1/2)
-  int dec_l2_ahead;          // decode producer prefetches the next 32 pages of an entry into L2
 };
-
-// 2^x on the FMA/ALU pipes (offloads MUFU.EX2 in the prefill softmax): x = n + f, 2^f by a cubic
-// with max relative error 8.6e-5 (P is stored as bf16: 3.9e-3), exponent added as integer bits.
-TC_DEVICE float exp2_poly3(float x) {
-  x = fmaxf(x, -126.f);
-  const float n = floorf(x);
-  const float f = x - n;
-  float p = fmaf(f, 0.0770652f, 0.227647f);
-  p = fmaf(p, f, 0.69511634f);
-  p = fmaf(p, f, 1.f);
-  return __int_as_float(__float_as_int(p) + ((int)n << 23));
-}
 
 TC_DEVICE void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -83,12 +66,6 @@ TC_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, 
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
-}
-// L2-only prefetch of one 3-D box (deepens the decode page stream beyond the smem ring).
-TC_DEVICE void tma_prefetch_3d_l2(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
 }
 TC_DEVICE void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -115,23 +92,6 @@ TC_DEVICE uint32_t kv_addr(uint32_t base, int key, int col, int v) {
 // Pool row of (page, layer, head, K, slot 0) for the 3-D tensor map.
 TC_DEVICE int kv_row(const AttnParams& p, int page, int head) {
   return (((page * p.n_layers + p.layer) * p.n_kv_heads + head) * 2) * kPage;
-}
-
-// Q fragment (A operand) of 16 rows: rows lo / hi -> (token, head).
-template <int DH>
-TC_DEVICE void attn_load_q(const AttnParams& p, int tok_lo, int head_lo, bool ok_lo, int tok_hi, int head_hi,
-                           bool ok_hi, uint32_t (&qf)[DH / 16][4]) {
-  const int qkv_ld = (p.n_heads + 2 * p.n_kv_heads) * DH;
-  const int lane = threadIdx.x % 32;
-  const __nv_bfloat16* qlo = p.qkv + (long long)tok_lo * qkv_ld + head_lo * DH + (lane % 4) * 2;
-  const __nv_bfloat16* qhi = p.qkv + (long long)tok_hi * qkv_ld + head_hi * DH + (lane % 4) * 2;
-#pragma unroll
-  for (int ks = 0; ks < DH / 16; ++ks) {
-    qf[ks][0] = ok_lo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16) : 0u;
-    qf[ks][1] = ok_hi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16) : 0u;
-    qf[ks][2] = ok_lo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + 8) : 0u;
-    qf[ks][3] = ok_hi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8) : 0u;
-  }
 }
 
 // S[16 x 8*NT] = Q K^T for keys [kbase, kbase + 8*NT) of the staged K blocks.
@@ -172,171 +132,6 @@ TC_DEVICE void attn_pv(const float (&pr)[NT][4], uint32_t v_smem, int kbase, flo
       mma_bf16_16816(o[n], a, b0, b1);
       mma_bf16_16816(o[n + 1], a, b2, b3);
     }
-  }
-}
-
-// Online-softmax update for one tile. Rows lane/4 (c0,c1) and lane/4+8 (c2,c3).
-// key_lim_lo/hi: exclusive key bound (absolute) for the two rows.
-template <int DH, int NT>
-TC_DEVICE void attn_softmax_step(float (&s)[NT][4], int key0, int key_lim_lo, int key_lim_hi, float scale_log2,
-                                 float (&m)[2], float (&l)[2], float (&o)[DH / 8][4]) {
-  const int lane = threadIdx.x % 32;
-  float mx[2] = {m[0], m[1]};
-#pragma unroll
-  for (int t = 0; t < NT; ++t) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int key = key0 + t * 8 + (lane % 4) * 2 + (e & 1);
-      const int lim = (e < 2) ? key_lim_lo : key_lim_hi;
-      float v = s[t][e] * scale_log2;
-      v = key < lim ? v : -INFINITY;
-      s[t][e] = v;
-      mx[e >> 1] = fmaxf(mx[e >> 1], v);
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-  }
-  float corr[2], rs[2] = {0.f, 0.f};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const float base = mx[h] == -INFINITY ? 0.f : mx[h];
-    corr[h] = exp2f(m[h] - base);  // m == -inf -> 0
-    m[h] = mx[h];
-    mx[h] = base;
-  }
-#pragma unroll
-  for (int t = 0; t < NT; ++t) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float pe = exp2f(s[t][e] - mx[e >> 1]);
-      s[t][e] = pe;
-      rs[e >> 1] += pe;
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) l[h] = l[h] * corr[h] + rs[h];
-#pragma unroll
-  for (int n = 0; n < DH / 8; ++n) {
-    o[n][0] *= corr[0];
-    o[n][1] *= corr[0];
-    o[n][2] *= corr[1];
-    o[n][3] *= corr[1];
-  }
-}
-
-// ============================================================== chunked prefill
-constexpr int kPrefillStages = 3;
-constexpr int kPrefillThreads = 160;  // 4 consumer warps + 1 TMA producer warp
-constexpr int kTilePages = 4;         // 64 keys per tile
-
-template <int DH>
-struct PrefillSmem {
-  static constexpr int kStageBytes = kTilePages * KvBlock<DH>::kPairBytes;  // 4 (K, V) page pairs
-  static constexpr int kBytes = kPrefillStages * kStageBytes + 1024;
-};
-
-template <int DH, int G>
-__global__ void __launch_bounds__(kPrefillThreads, 2) attn_prefill(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  constexpr int TPW = 16 / G;  // tokens per warp
-  constexpr int TPC = 4 * TPW;
-  constexpr int kKeys = kTilePages * kPage;
-  extern __shared__ uint8_t attn_smem_raw[];
-  __shared__ uint64_t full_bar[kPrefillStages], empty_bar[kPrefillStages];
-  const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int seq = p.qblk_seq[blockIdx.x];
-  const int qoff = p.qblk_off[blockIdx.x];
-  const int kvh = blockIdx.y;
-  const int q_start = p.seq_q_start[seq], q_len = p.seq_q_len[seq], pos0 = p.seq_pos0[seq];
-  const int* bt = p.block_tables + p.seq_bt_off[seq];
-  const int kv_end = pos0 + min(qoff + TPC, q_len);
-  const int n_tiles = (kv_end + kKeys - 1) / kKeys;
-  const int n_pages = (kv_end + kPage - 1) / kPage;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kPrefillStages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 4);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  if (warp == 4) {
-    // ---------------- TMA producer: 4 K blocks + 4 V blocks per tile. Lanes 0-3 fetch the
-    // next tile's page ids while lane 0 issues the current tile, so block-table latency never
-    // sits between two TMA issues.
-    auto page_id = [&](int gp) { return bt[gp < n_pages ? gp : 0]; };  // beyond the sequence: any page, masked
-    int cur = lane < kTilePages ? page_id(lane) : 0;
-    if (lane == 0) tma_prefetch_desc(&kv_map);
-    for (int t = 0; t < n_tiles; ++t) {
-      int ids[kTilePages];
-#pragma unroll
-      for (int pg = 0; pg < kTilePages; ++pg) ids[pg] = __shfl_sync(0xffffffffu, cur, pg);
-      if (lane < kTilePages && t + 1 < n_tiles) cur = page_id((t + 1) * kTilePages + lane);
-      if (lane == 0) {
-        const int st = t % kPrefillStages;
-        mbar_wait(&empty_bar[st], ((t / kPrefillStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full_bar[st], PrefillSmem<DH>::kStageBytes);
-        const uint32_t dst = sbase + st * PrefillSmem<DH>::kStageBytes;
-#pragma unroll
-        for (int pg = 0; pg < kTilePages; ++pg) {
-          tma_load_3d(dst + pg * KvBlock<DH>::kPairBytes, &kv_map, &full_bar[st], KV_COORD(kv_row(p, ids[pg], kvh)));
-        }
-      }
-      __syncwarp();
-    }
-    return;
-  }
-
-  // ---------------- consumers: rows of this warp: r -> token r / G, head r % G
-  const int r_lo = lane / 4, r_hi = lane / 4 + 8;
-  const int tl_lo = qoff + warp * TPW + r_lo / G, tl_hi = qoff + warp * TPW + r_hi / G;
-  const bool ok_lo = r_lo < TPW * G && tl_lo < q_len;
-  const bool ok_hi = r_hi < TPW * G && tl_hi < q_len;
-  const int head_lo = kvh * G + r_lo % G, head_hi = kvh * G + r_hi % G;
-  uint32_t qf[DH / 16][4];
-  attn_load_q<DH>(p, q_start + (ok_lo ? tl_lo : 0), head_lo, ok_lo, q_start + (ok_hi ? tl_hi : 0), head_hi, ok_hi, qf);
-  const int lim_lo = ok_lo ? pos0 + tl_lo + 1 : 0;  // causal: query at pos0+tl sees keys <= pos0+tl
-  const int lim_hi = ok_hi ? pos0 + tl_hi + 1 : 0;
-
-  float o[DH / 8][4];
-#pragma unroll
-  for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-
-  for (int t = 0; t < n_tiles; ++t) {
-    const int st = t % kPrefillStages;
-    mbar_wait(&full_bar[st], (t / kPrefillStages) & 1);
-    const uint32_t k_smem = sbase + st * PrefillSmem<DH>::kStageBytes;
-    const uint32_t v_smem = k_smem;  // kv_addr selects the V rows
-    float s[8][4];
-    attn_qk<DH, 8>(qf, k_smem, 0, s);
-    attn_softmax_step<DH, 8>(s, t * kKeys, lim_lo, lim_hi, p.scale_log2, m, l, o);
-    attn_pv<DH, 8>(s, v_smem, 0, o);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[st]);
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 1);
-    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 2);
-  }
-  const int out_ld = p.n_heads * DH;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const bool ok = h ? ok_hi : ok_lo;
-    if (!ok) continue;
-    const int tok = q_start + (h ? tl_hi : tl_lo);
-    const int head = h ? head_hi : head_lo;
-    const float inv = 1.f / l[h];
-    __nv_bfloat16* dst = p.out + (long long)tok * out_ld + head * DH + (lane % 4) * 2;
-#pragma unroll
-    for (int n = 0; n < DH / 8; ++n)
-      *reinterpret_cast<uint32_t*>(dst + n * 8) = pack_bf16(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
   }
 }
 
@@ -568,24 +363,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const float base = m_used == -INFINITY ? 0.f : m_used;
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[32];
-      if (full && p.pf_poly == 2) {
-#pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
-          const float p1 = exp2_poly3(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base));
-          sum4[x & 3] += p0 + p1;
-          pk[x] = pack_bf16(p0, p1);
-        }
-      } else if (full && p.pf_poly == 1) {
-#pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
-          const float s1 = fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base);
-          const float p1 = (x & 1) ? exp2_poly3(s1) : fast_exp2(s1);
-          sum4[x & 3] += p0 + p1;
-          pk[x] = pack_bf16(p0, p1);
-        }
-      } else if (full) {
+      if (full) {
 #pragma unroll
         for (int x = 0; x < 32; ++x) {
           const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
@@ -653,30 +431,37 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 // mix. A CTA's range is a list of ENTRIES (segment, page0, page1, part).
 //
 // Inside a CTA: one producer warp walks the entries and streams each page's K and V blocks
-// (2 TMA loads, 8 KiB at head_dim 128) into a deep ring, plus the segment's q rows (one bulk
+// (one TMA box, 8 KiB at head_dim 128) into the ring, plus the segment's q rows (one bulk
 // copy per entry) into a double-buffered q slot; it never waits for a consumer except on a
-// full ring. Consumer warp w takes ring stages w, w+4, w+8, ... and keeps its own online-
-// softmax state per entry; at the end of an entry the 4 partial states meet in shared memory
-// (one named barrier) and warp (entry % 4) merges them. Only segments cut by a CTA boundary
+// full ring. Consumer warp w takes ring stages w, w+NC, w+2NC, ... and keeps its own online-
+// softmax state per entry; at the end of an entry the NC partial states meet in shared memory
+// (one named barrier) and warp (entry % NC) merges them. Only segments cut by a CTA boundary
 // (at most 2 per CTA) go through global memory: the merging warp writes its partial, and the
 // CTA that arrives last on the segment's counter combines the parts.
-constexpr int kDecConsumers = 4;
+//
+// The consumers, not the ring, set the page rate (round 1: 4 warps at ~1,200 cycles per page
+// each = ~40 GB/s per SM, a quarter of the samples waiting on a full barrier): 8 consumer warps
+// over a 128 KiB ring, and a page costs ~110 instructions -- 16 + 16 mma.sync, 16 ldmatrix, the
+// key mask only on a segment's last page, and a lazy softmax base (the base, and with it l and o,
+// moves only when a row's max grows by more than 2^8, which after the first page is rare).
+constexpr int kDecConsumers = 8;
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;
-constexpr int kDecRingBytes = 192 * 1024;
+constexpr int kDecRingBytes = 128 * 1024;
+constexpr float kDecRescaleLog2 = 8.f;  // lazy base: p = 2^(s - base) <= 2^8, P stays in bf16 range
 
-template <int DH, int G, int RING = kDecRingBytes>
+template <int DH, int G>
 struct DecodeSmem {
   static constexpr int kStageBytes = KvBlock<DH>::kPairBytes;  // one page-head: K block then V block
-  static constexpr int kStages = RING / kStageBytes;
+  static constexpr int kStages = kDecRingBytes / kStageBytes;
   static constexpr int kQBytes = G * DH * 2;
   static constexpr int kPartFloats = kDecConsumers * G * DH;  // per buffer
-  static constexpr int kOffQ = RING;
+  static constexpr int kOffQ = kDecRingBytes;
   static constexpr int kOffPart = kOffQ + 2 * ((kQBytes + 127) / 128 * 128);
   static constexpr int kOffMl = kOffPart + 2 * kPartFloats * 4;
   static constexpr int kBytes = kOffMl + 2 * kDecConsumers * G * 2 * 4 + 1024;
-  // Stage g is consumed by warp g % 4. With S a multiple of 4 every slot has ONE owner warp, which
-  // waits for use k+1 only after finishing use k; otherwise a warp running a lap ahead could pass
-  // a parity wait on a phase that has not landed yet (mbarrier parity ABA).
+  // Stage g is consumed by warp g % NC. With S a multiple of NC every slot has ONE owner warp,
+  // which waits for use k+1 only after finishing use k; otherwise a warp running a lap ahead
+  // could pass a parity wait on a phase that has not landed yet (mbarrier parity ABA).
   static_assert(kStages % kDecConsumers == 0, "decode ring: stages must be a multiple of the consumer warps");
   static_assert(kBytes <= 227 * 1024, "decode smem");
 };
@@ -736,12 +521,61 @@ TC_DEVICE void store_out_row(__nv_bfloat16* out_row, const float (&acc)[G][DH / 
   }
 }
 
-// RING < 192 KB: smaller ring, two CTAs per SM (twice the consumer warps per SM; A/B TC_DEC_2CTA)
-template <int DH, int G, int RING = kDecRingBytes>
-__global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
-    attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  using SM = DecodeSmem<DH, G, RING>;
+// One page of one consumer warp: S = q K^T over the page's 16 keys (rows lane/4 and lane/4 + 8 of
+// the 16-row fragment; rows >= G carry zero q), lazy-base online softmax, O += P V.
+template <int DH>
+TC_DEVICE void dec_page(const uint32_t (&qf)[DH / 16][4], uint32_t kv_smem, int key0, int kv_len, float scale_log2,
+                        float (&m)[2], float (&l)[2], float (&o)[DH / 8][4]) {
+  const int lane = threadIdx.x % 32;
+  float s[2][4];
+  attn_qk<DH, 2>(qf, kv_smem, 0, s);
+  if (key0 + kPage > kv_len) {  // the segment's last page (warp-uniform)
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (key0 + t * 8 + (lane % 4) * 2 + (e & 1) >= kv_len) s[t][e] = -INFINITY;
+  }
+  float mx[2] = {fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1])),
+                 fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]))};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+    mx[h] *= scale_log2;  // scale > 0: the max commutes with it (-inf stays -inf)
+  }
+  // every page holds at least one valid key, so mx is finite; m == -inf only before the first page
+  const bool grow = mx[0] > m[0] + kDecRescaleLog2 || mx[1] > m[1] + kDecRescaleLog2;
+  if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float nb = fmaxf(m[h], mx[h]);
+      const float corr = exp2f(m[h] - nb);  // m == -inf -> 0
+      m[h] = nb;
+      l[h] *= corr;
+#pragma unroll
+      for (int n = 0; n < DH / 8; ++n) {
+        o[n][2 * h] *= corr;
+        o[n][2 * h + 1] *= corr;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float pe = exp2f(fmaf(s[t][e], scale_log2, -m[e >> 1]));
+      s[t][e] = pe;
+      l[e >> 1] += pe;
+    }
+  attn_pv<DH, 2>(s, kv_smem, 0, o);
+}
+
+template <int DH, int G>
+__global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  using SM = DecodeSmem<DH, G>;
   constexpr int S = SM::kStages;
+  constexpr int NC = kDecConsumers;
   constexpr int V = DH / 32;
   extern __shared__ uint8_t attn_smem_raw[];
   __shared__ uint64_t full[S], empty[S], qfull[2], qempty[2];
@@ -756,7 +590,7 @@ __global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&qfull[b], 1);
-      mbar_init(&qempty[b], kDecConsumers);
+      mbar_init(&qempty[b], NC);
     }
     mbar_fence_init();
   }
@@ -765,7 +599,7 @@ __global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
   pdl_trigger();
   const int qkv_ld = (p.n_heads + 2 * p.n_kv_heads) * DH;
 
-  if (warp == kDecConsumers) {
+  if (warp == NC) {
     // ------------------------------------------------------------ producer
     if (lane == 0) tma_prefetch_desc(&kv_map);
     int g = 0;  // stages issued
@@ -792,10 +626,6 @@ __global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
         for (int c = pg0; c < pg1; c += 32) {
           // lane j: pool row of page c + j (coordinates computed 32 at a time, off the issue path)
           const int row = c + lane < pg1 ? kv_row(p, p.block_tables[bt_off + c + lane], kvh) : 0;
-          // the entry's next 32 pages into L2 (one prefetch per lane): keeps ~2x the ring's bytes
-          // in flight per SM, the decode stream being bound by per-SM outstanding bytes
-          if (p.dec_l2_ahead && c + 32 + lane < pg1)
-            tma_prefetch_3d_l2(&kv_map, KV_COORD(kv_row(p, p.block_tables[bt_off + c + 32 + lane], kvh)));
           const int n = min(32, pg1 - c);
           for (int j = 0; j < n; ++j, ++g) {
             const int rj = __shfl_sync(0xffffffffu, row, j);
@@ -857,38 +687,34 @@ __global__ void __launch_bounds__(kDecThreads, RING < 128 * 1024 ? 2 : 1)
       for (int c = 0; c < DH / 8; ++c) o[c][0] = o[c][1] = o[c][2] = o[c][3] = 0.f;
       float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
       const int n = pg1 - pg0;
-      // this warp's stages of the entry: g_base + i with (g_base + i) % 4 == warp
-      for (int i = (warp - g_base % kDecConsumers + kDecConsumers) % kDecConsumers; i < n; i += kDecConsumers) {
+      // this warp's stages of the entry: g_base + i with (g_base + i) % NC == warp
+      for (int i = (warp - g_base % NC + NC) % NC; i < n; i += NC) {
         const int g = g_base + i;
         const int st = g % S;
         mbar_wait(&full[st], (g / S) & 1);
-        const uint32_t k_smem = sbase + st * SM::kStageBytes;
-        float s[2][4];
-        attn_qk<DH, 2>(qf, k_smem, 0, s);
-        attn_softmax_step<DH, 2>(s, (pg0 + i) * kPage, kv_len, kv_len, p.scale_log2, m, l, o);
-        attn_pv<DH, 2>(s, k_smem, 0, o);
+        dec_page<DH>(qf, sbase + st * SM::kStageBytes, (pg0 + i) * kPage, kv_len, p.scale_log2, m, l, o);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
       }
       g_base += n;
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], 1);
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], 2);
-      // publish this warp's partial state
-      float* po = part_o + ((b * kDecConsumers + warp) * G) * DH;
-      float* pml = part_ml + ((b * kDecConsumers + warp) * G) * 2;
+      // publish this warp's partial state (a warp without pages publishes m = -inf, l = 0, o = 0)
+      float* po = part_o + ((b * NC + warp) * G) * DH;
+      float* pml = part_ml + ((b * NC + warp) * G) * 2;
       if (ok_lo) {
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(po + r_lo * DH + c * 8 + c0) = make_float2(o[c][0], o[c][1]);
         if (lane % 4 == 0) *reinterpret_cast<float2*>(pml + r_lo * 2) = make_float2(m[0], l[0]);
       }
       consumer_bar();
-      if (warp != e % kDecConsumers) continue;
-      // merging warp: combine the 4 warps' states of this entry
-      const float* bo = part_o + (b * kDecConsumers * G) * DH;
-      const float* bml = part_ml + (b * kDecConsumers * G) * 2;
+      if (warp != e % NC) continue;
+      // merging warp: combine the NC warps' states of this entry
+      const float* bo = part_o + (b * NC * G) * DH;
+      const float* bml = part_ml + (b * NC * G) * 2;
       float acc[G][V], mm[G], ll[G];
       merge_partials<DH, G>(
-          kDecConsumers, [&](int j, int r) { return *reinterpret_cast<const float2*>(bml + (j * G + r) * 2); },
+          NC, [&](int j, int r) { return *reinterpret_cast<const float2*>(bml + (j * G + r) * 2); },
           [&](int j, int r, float* d) {
             const float* src = bo + (j * G + r) * DH + lane * V;
 #pragma unroll

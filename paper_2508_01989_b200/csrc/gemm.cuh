@@ -83,14 +83,9 @@ struct GemmArgs {
                              // zeroed fp32 [M, N] scratch; a finish kernel applies the epilogue
   int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
   int stages;                // gemm_ws_2sm: smem ring depth for this token tile
-  unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][8]
-  int rope_stage;            // gemm_ws_2sm QKV epilogue: stage (cos, sin) rows in the idle ring
-  int dbg;                   // gemm_ws_2sm (tools only, TC_WS_DBG): 1 skip the row-phase stores,
-                             // 2 skip the row phase, 3 skip staging + row phase
-  // gemm_ws_2sm: plan of the next GEMM of the step (its first k-blocks are prefetched into L2)
-  int nx_on, nx_m_tiles, nx_splits, nx_kb, nx_units, nx_streamk, nx_pairs, nx_stages, nx_total;
-  int streamk;               // gemm_ws_2sm, residual epilogue: pair p takes k-blocks
-                             // [W p / P, W (p+1) / P) of the tile-major stream (W = tiles * kb)
+  unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][16]
+  int streamk;               // gemm_ws_2sm, residual epilogue: grouped stream-K (gemm_ws.cuh WsIter)
+  int groups;                // gemm_ws_2sm stream-K: pair groups (m_tiles sibling pairs each)
 };
 
 template <int BN>
@@ -612,204 +607,6 @@ __global__ void finish_qkv_rope(float* __restrict__ scr, int M, QkvRopeArgs r, c
                                       pack_bf16(lo[6], lo[7])));
     st_global_v4(dst + j0 + half, make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
                                              pack_bf16(hi[6], hi[7])));
-  }
-}
-
-// ---------------------------------------------------------------- 2-SM variant
-// CTA pair (cluster 2x1) computes a 256 x 256 tile with tcgen05.mma.cta_group::2: each CTA
-// loads its 128 rows of A and 128 rows of B per k-block (32 KB instead of 48 KB for a
-// single-SM 128 x 256 tile), and accumulates its 128 x 256 half in its own TMEM. The per-SM
-// L2->SMEM fill rate, which bounds the single-SM kernel at ~15 TB/s aggregate, drops by a
-// third. Leader (rank 0) issues the MMAs; both CTAs' TMA credit the leader's full barrier;
-// commits multicast to both CTAs' empty / accumulator-full barriers; both epilogues release
-// the accumulator on the leader's barrier. Splits only via red.add (RESID / streaming).
-constexpr int kGemm2BN = 256;      // pair tile N (each CTA loads 128 rows of B)
-constexpr int kGemm2Stages = 6;    // 6 x 32 KB
-struct Gemm2Cfg {
-  static constexpr int kABytes = 128 * kGemmBK * 2;
-  static constexpr int kBBytes = 128 * kGemmBK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmemBytes = kGemm2Stages * kStageBytes + 1024 + 512;
-};
-
-template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                          GemmArgs args) {
-  constexpr int BN = kGemm2BN;
-  constexpr int S = kGemm2Stages;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + S * Gemm2Cfg::kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Gemm2Cfg::kStageBytes);
-  uint64_t* empty_bar = full_bar + S;
-  uint64_t* tfull_bar = empty_bar + S;   // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;  // [2] (leader's copy is used)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-
-  const int warp = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  // args.m_tiles counts 256-row pair tiles here
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&map_a);
-    tma_prefetch_desc(&map_b);
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs
-    }
-    mbar_fence_init();
-  }
-  if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
-  tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised before any cross-CTA arrive / TMA credit
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // predecessor kernel's outputs (activations, residual) are visible from here on
-  pdl_trigger();
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = pair; u < args.units; u += n_pairs) {
-        const Unit w = unit_of(args, u);
-        for (int kb = w.k0; kb < w.k1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Gemm2Cfg::kStageBytes);
-          tma_load_2d_2sm(smem_a + stage * Gemm2Cfg::kABytes, &map_a, &full_bar[stage], kb * kGemmBK,
-                          w.mt * 256 + (int)rank * 128, kEvictLast);
-          tma_load_2d_2sm(smem_b + stage * Gemm2Cfg::kBBytes, &map_b, &full_bar[stage], kb * kGemmBK,
-                          w.nt * BN + (int)rank * 128, kEvictNormal);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (rank == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int u = pair; u < args.units; u += n_pairs) {
-        const Unit w = unit_of(args, u);
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        ++local;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = w.k0; kb < w.k1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t a_addr = smem_u32(smem_a + stage * Gemm2Cfg::kABytes);
-            const uint32_t b_addr = smem_u32(smem_b + stage * Gemm2Cfg::kBBytes);
-#pragma unroll
-            for (int k = 0; k < kGemmBK / 16; ++k)
-              umma_bf16_2sm(d_tmem, umma_smem_desc<kGemmBK * 2>(a_addr + k * 32),
-                            umma_smem_desc<kGemmBK * 2>(b_addr + k * 32), idesc, (kb > w.k0 || k > 0) ? 1u : 0u);
-            umma_commit_2sm_multicast(&empty_bar[stage]);
-            if (kb == w.k1 - 1) umma_commit_2sm_multicast(&tfull_bar[acc]);
-          }
-          __syncwarp();
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    const int ew = warp - 4;
-    const int row = ew * 32 + lane;
-    int local = 0;
-    for (int u = pair; u < args.units; u += n_pairs) {
-      const Unit w = unit_of(args, u);
-      const int nt = w.nt;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      ++local;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const int m = w.mt * 256 + (int)rank * 128 + row;
-      const bool row_ok = m < args.M;
-      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-      if (args.red_out != nullptr) {
-#pragma unroll 1
-        for (int chunk = 0; chunk < BN / 32; ++chunk) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + chunk * 32, r);
-          tmem_ld_wait();
-          if (row_ok) {
-            float* dst = args.red_out + (size_t)m * args.N + nt * BN + chunk * 32;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + q * 4),
-                           "f"(__uint_as_float(r[q * 4])), "f"(__uint_as_float(r[q * 4 + 1])),
-                           "f"(__uint_as_float(r[q * 4 + 2])), "f"(__uint_as_float(r[q * 4 + 3]))
-                           : "memory");
-          }
-        }
-      } else if constexpr (EPI == EPI_QKV_ROPE) {
-        auto fetch = [&](int chunk, float (&v)[32]) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + chunk * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        };
-        epi_qkv_rope_row<BN>(args, m, row_ok, nt, fetch);
-      } else if constexpr (EPI == EPI_SWIGLU) {
-#pragma unroll 1
-        for (int grp = 0; grp < BN / 128; ++grp) {
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            uint32_t gr[32], ur[32];
-            tmem_ld_32x32b_x32(t_row + grp * 128 + half * 32, gr);
-            tmem_ld_32x32b_x32(t_row + grp * 128 + 64 + half * 32, ur);
-            tmem_ld_wait();
-            float g[32], uu[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              g[i] = __uint_as_float(gr[i]);
-              uu[i] = __uint_as_float(ur[i]);
-            }
-            if (row_ok) epi_swiglu_chunk(args, m, (nt * BN) / 2 + grp * 64 + half * 32, g, uu);
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int chunk = 0; chunk < BN / 32; ++chunk) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + chunk * 32, r);
-          tmem_ld_wait();
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (row_ok) epi_store_chunk<BN, EPI>(args, m, nt * BN + chunk * 32, v);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync();  // every MMA retired and both epilogues drained before TMEM is released
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc_2sm(tmem_base, 2 * BN);
   }
 }
 

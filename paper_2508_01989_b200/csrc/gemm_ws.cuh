@@ -62,7 +62,7 @@ __device__ __forceinline__ float4 ws_ld4(const float* sb, int t, int ch) {
 // starting at global weight row fbase.
 template <int EPI>
 __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const float* sb, int t, int s, int tok, int fbase,
-                                                int pos, int kv_row, const float2* cs_stage = nullptr) {
+                                                int pos, int kv_row) {
   if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_BIAS) {
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)tok * args.ldo + fbase + s * 32;
 #pragma unroll
@@ -150,8 +150,7 @@ __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const floa
       }
     }
     if (is_q || is_k) {
-      // (cos, sin) of this row: staged in smem by the epilogue (single-unit launches) or global
-      const float2* cs = cs_stage ? cs_stage + j0 : r.rope_cs + (size_t)pos * half + j0;
+      const float2* cs = r.rope_cs + (size_t)pos * half + j0;  // (cos, sin) of this row
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {
         const float4 c = *reinterpret_cast<const float4*>(cs + i);  // (cos, sin) x 2
@@ -176,20 +175,24 @@ __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const floa
 }
 
 // Work iterator shared by the producer, MMA and epilogue roles of one pair (identical sequences).
-// Default: units u = pair, pair + n_pairs, ... (tile, k-split). Stream-K (residual epilogue, where
-// every partial is a TMA bulk add): the pair's contiguous range of the tile-major k-block stream,
-// cut at tile boundaries -- equal k-blocks per pair whatever the tile count (decode-only steps:
-// 112 gate_up tiles on 74 pairs would otherwise leave half the pairs a second full tile).
+// Default: units u = pair, pair + n_pairs, ... (tile, k-split). Grouped stream-K (residual
+// epilogue, where every partial is a TMA bulk add): pair p is token tile p % m_tiles of group
+// p / m_tiles; group g takes the contiguous range [W g / G, W (g+1) / G) of the weight-tile-major
+// k-block stream (W = n_tiles * kb), cut at weight-tile boundaries. The m_tiles siblings of a
+// group issue the same weight k-blocks at the same time (one DRAM read, the rest hit L2), and
+// every pair gets the same number of k-blocks whatever the tile count.
 struct WsIter {
   long long pos, end;  // stream-K
-  int u;               // units
+  int u, mt;           // units / stream-K token tile
 };
 __device__ __forceinline__ WsIter ws_iter_begin(const GemmArgs& a, int pair, int n_pairs) {
   WsIter it;
   it.u = pair;
-  const long long total = (long long)a.m_tiles * a.n_tiles * a.kb;
-  it.pos = total * pair / n_pairs;
-  it.end = total * (pair + 1) / n_pairs;
+  it.mt = pair % a.m_tiles;
+  const int grp = pair / a.m_tiles;
+  const long long total = (long long)a.n_tiles * a.kb;
+  it.pos = total * grp / a.groups;
+  it.end = total * (grp + 1) / a.groups;
   return it;
 }
 __device__ __forceinline__ bool ws_next(const GemmArgs& a, WsIter& it, int n_pairs, Unit& w) {
@@ -203,8 +206,8 @@ __device__ __forceinline__ bool ws_next(const GemmArgs& a, WsIter& it, int n_pai
   const int tile = (int)(it.pos / a.kb);
   w.k0 = (int)(it.pos - (long long)tile * a.kb);
   w.k1 = (int)min((long long)a.kb, w.k0 + (it.end - it.pos));
-  w.mt = tile % a.m_tiles;
-  w.nt = tile / a.m_tiles;
+  w.mt = it.mt;
+  w.nt = tile;
   w.ks = 0;
   it.pos += w.k1 - w.k0;
   return true;
@@ -218,7 +221,7 @@ __device__ __forceinline__ bool ws_next(const GemmArgs& a, WsIter& it, int n_pai
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
     gemm_ws_2sm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_next, GemmArgs args) {
+                const __grid_constant__ CUtensorMap map_o, GemmArgs args) {
   const int TN = args.tn, S = args.stages;
   const int stage_bytes = ws_stage_bytes(TN);
   extern __shared__ uint8_t smem_raw[];
@@ -299,11 +302,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
             if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_bytes);
             tma_load_2d_2sm(st, &map_w, &full_bar[stage], kb * kGemmBK, w.nt * 256 + wrow, kEvictNormal);
           }
-#if TC_WS_L2_PREFETCH
-          // keep the DRAM weight stream a ring's depth further ahead through L2 (off: it wins in the
-          // isolated microbench but costs 3% in the step, where L2 also holds the activations)
-          if (kb + S < w.k1) tma_prefetch_2d_l2(&map_w, (kb + S) * kGemmBK, w.nt * 256 + wrow);
-#endif
           tma_load_2d_2sm(st + kWsWBytes, &map_x, &full_bar[stage], kb * kGemmBK, w.mt * TN + (int)rank * half_tn,
                           kEvictLast);
           if (++stage == S) {
@@ -311,28 +309,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
             phase ^= 1;
           }
         }
-      }
-      // all own loads issued: pull the next GEMM's first weight k-blocks for the same pair index
-      // into L2 (that kernel's pipeline fill then hits L2, not DRAM)
-      if (args.nx_on && pair < args.nx_pairs) {
-        int nt, k0, k1;
-        if (args.nx_streamk) {  // the pair's range of the tile-major k-block stream (ws_iter_begin)
-          const long long pos = (long long)args.nx_total * pair / args.nx_pairs;
-          const int tile = (int)(pos / args.nx_kb);
-          nt = tile / args.nx_m_tiles;
-          k0 = (int)(pos - (long long)tile * args.nx_kb);
-          k1 = min(args.nx_kb, k0 + args.nx_stages);
-        } else {
-          GemmArgs nx = args;
-          nx.m_tiles = args.nx_m_tiles;
-          nx.splits = args.nx_splits;
-          nx.kb = args.nx_kb;
-          const Unit u0 = unit_of(nx, pair);
-          nt = u0.nt;
-          k0 = u0.k0;
-          k1 = min(u0.k1, u0.k0 + args.nx_stages);
-        }
-        for (int kb = k0; nt >= 0 && kb < k1; ++kb) tma_prefetch_2d_l2(&map_next, kb * kGemmBK, nt * 256 + wrow);
       }
     }
   } else if (warp == 1) {
@@ -416,24 +392,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (et == 0 && grp == 0) stamp(7);
-      // single-unit launch (every pair owns one unit, e.g. QKV at T=576): the MMAs are done and the
-      // ring is idle, so stage this unit's (cos, sin) rows in it with one round of independent 16 B
-      // loads instead of one dependent L2 round trip per 32-token chunk
-      const float2* cs_stage = nullptr;
-      if constexpr (EPI == EPI_QKV_ROPE) {
-        if (args.rope_stage) {
-          const int half = args.rope.head_dim >> 1, cpr = half / 2;  // 16 B chunks per row
-          float4* dst = reinterpret_cast<float4*>(smem);
-          const int e2 = threadIdx.x - 128;
-          for (int k = e2; k < TN * cpr; k += 256) {
-            const int tl = k / cpr, c = k - tl * cpr;
-            if (w.mt * TN + tl < args.M)
-              dst[k] = __ldg(reinterpret_cast<const float4*>(args.rope.rope_cs + (size_t)mpos[tl] * half) + c);
-          }
-          asm volatile("bar.sync 3, 256;" ::: "memory");
-          cs_stage = reinterpret_cast<const float2*>(smem);
-        }
-      }
       const int fbase = w.nt * 256 + (int)rank * 128;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
       const int my_last = (n_chunks - 1 - grp) >= 0 ? ((n_chunks - 1 - grp) & ~1) + grp : -1;
@@ -468,21 +426,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
             tma_reduce_add_2d(&map_o, smem_u32(sb), fbase, tok0);
             bulk_commit_group();
           }
-        } else if (args.dbg != 3) {
+        } else {
           asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");  // previous row phase done with sb
 #pragma unroll
           for (int i = 0; i < 32; ++i) sb[ws_stg_idx(i, fch) + fe] = __uint_as_float(r[i]);
           asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
           const int tok = w.mt * TN + c0 + t;
-          if (args.dbg == 1) {  // tools only: read the staged row, skip the global stores
-            float acc = 0.f;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc += ws_ld4(sb, t, s * 8 + q).x;
-            if (acc == 123456.f) args.trace[0] = 1;
-          } else if (args.dbg != 2 && tok < args.M) {
-            ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t],
-                                 cs_stage ? cs_stage + (size_t)(c0 + t) * (args.rope.head_dim >> 1) : nullptr);
-          }
+          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
         }
         if (et == 0 && grp == 0 && ci < 6) stamp(9 + ci);      // 9, 11, 13: chunk done
       }

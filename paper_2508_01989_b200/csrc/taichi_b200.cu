@@ -189,28 +189,16 @@ void init_kernel_attrs(int dev) {
   TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
   TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
   TC_CUDA(cudaFuncSetAttribute(tc::gemm_ws_2sm<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kWsSmemBytes));
-  // attention kernels run 2 CTAs/SM (~97 KB each): ask for the maximum shared-memory carveout,
-  // otherwise the driver's default split leaves room for only one (ncu: occupancy 7.8%)
-  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
-  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
-  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
-  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
-  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
-  TC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16_tcgen05_2sm<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Gemm2Cfg::kSmemBytes));
+  // attention kernels: maximum shared-memory carveout (the driver's default split is smaller)
   auto attr = [](const void* fn, int bytes) {
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   };
-  attr((const void*)tc::attn_prefill<64, 2>, tc::PrefillSmem<64>::kBytes);
-  attr((const void*)tc::attn_prefill<128, 4>, tc::PrefillSmem<128>::kBytes);
-  attr((const void*)tc::attn_prefill<128, 5>, tc::PrefillSmem<128>::kBytes);
   attr((const void*)tc::attn_prefill_tc<64, 2>, tc::PfCfg<64, 2>::kBytes);
   attr((const void*)tc::attn_prefill_tc<128, 4>, tc::PfCfg<128, 4>::kBytes);
   attr((const void*)tc::attn_prefill_tc<128, 5>, tc::PfCfg<128, 5>::kBytes);
   attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64, 2>::kBytes);
   attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128, 4>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 96 * 1024>, tc::DecodeSmem<128, 4, 96 * 1024>::kBytes);
-  attr((const void*)tc::attn_decode<128, 5, 96 * 1024>, tc::DecodeSmem<128, 5, 96 * 1024>::kBytes);
   attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128, 5>::kBytes);
   done.insert(dev);
 }
@@ -345,23 +333,6 @@ struct SkWorkspace {
   int* cnt = nullptr;
 };
 
-// 2-SM (CTA pair) GEMM: 256 x 256 tiles, tcgen05.mma.cta_group::2. Used for M > kGemm2MinM.
-constexpr int kGemm2MinM = 1 << 30;  // set after measurement (tools/gemm_bench.py, bn = 512 forces it)
-
-void launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb128, const tc::GemmArgs& args, int epi, int grid,
-                     cudaStream_t s) {
-  const int smem = tc::Gemm2Cfg::kSmemBytes;
-  switch (epi) {
-    case tc::EPI_BF16: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
-    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_BF16_BIAS>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
-    case tc::EPI_RESID_F32: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_RESID_F32>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
-    case tc::EPI_SWIGLU: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_SWIGLU>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
-    case tc::EPI_F32: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_F32>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
-    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_bf16_tcgen05_2sm<tc::EPI_QKV_ROPE>, grid, tc::kGemmThreads, smem, s, ma, mb128, args); break;
-    default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
-  }
-}
-
 // Weight-stationary pair kernel (gemm_ws.cuh) for mixed / prefill steps: T > kWsMinRows rows,
 // weight rows a multiple of 256. TC_GEMM_WS=0 in the environment falls back to the token-major
 // kernels (A/B switch for measurement).
@@ -374,40 +345,25 @@ bool ws_enabled() {
   return on;
 }
 
-void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensorMap& mo, const CUtensorMap& mn,
-                    const tc::GemmArgs& args, int epi, int grid, cudaStream_t s) {
+void launch_gemm_ws(const CUtensorMap& mw, const CUtensorMap& mx, const CUtensorMap& mo, const tc::GemmArgs& args, int epi,
+                    int grid, cudaStream_t s) {
   const int smem = tc::kWsSmemBytes;
   switch (epi) {
-    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
-    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
-    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
-    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
-    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
-    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kWsThreads, smem, s, mw, mx, mo, mn, args); break;
+    case tc::EPI_BF16: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_BF16_BIAS: launch_k(tc::gemm_ws_2sm<tc::EPI_BF16_BIAS>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_RESID_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_RESID_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_SWIGLU: launch_k(tc::gemm_ws_2sm<tc::EPI_SWIGLU>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_F32: launch_k(tc::gemm_ws_2sm<tc::EPI_F32>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
+    case tc::EPI_QKV_ROPE: launch_k(tc::gemm_ws_2sm<tc::EPI_QKV_ROPE>, grid, tc::kWsThreads, smem, s, mw, mx, mo, args); break;
     default: throw TcFail{TC_ERR_INVALID, "unsupported gemm epilogue"};
   }
 }
 
-// The GEMM that follows in the step (its weights' first k-blocks are pulled into L2 by the
-// current GEMM's producer once it has issued its own loads: the next kernel's pipeline fill then
-// comes from L2 instead of DRAM).
-struct NextGemm {
-  const WMat* w = nullptr;
-  int M = 0, epi = 0;
-};
-
-// Tiling / split / stream-K plan of a weight-stationary GEMM (shared by the launch and by the
-// previous GEMM's L2 prefetch of this one).
+// Tiling / split / stream-K plan of a weight-stationary GEMM.
 tc::GemmArgs plan_gemm_ws(int M, int N, int K, int epi, int sms, int force_splits) {
   tc::GemmArgs args{};
-  // token tiles: the fewest that keep TN <= 256 (each extra tile re-reads the weights);
-  // TC_WS_NTT_RESID=n forces n for the residual GEMMs (measurement knob)
-  static const int ntt_resid = [] {
-    const char* e = std::getenv("TC_WS_NTT_RESID");
-    return e ? std::atoi(e) : 0;
-  }();
-  int n_tt = (M + 255) / 256;
-  if (epi == tc::EPI_RESID_F32 && ntt_resid > n_tt && (M + ntt_resid - 1) / ntt_resid >= 16) n_tt = ntt_resid;
+  // token tiles: the fewest that keep TN <= 256 (each extra tile re-reads the weights)
+  const int n_tt = (M + 255) / 256;
   args.tn = ((M + n_tt - 1) / n_tt + 31) / 32 * 32;
   args.stages = tc::ws_stages(args.tn);
   args.M = M;
@@ -418,12 +374,23 @@ tc::GemmArgs plan_gemm_ws(int M, int N, int K, int epi, int sms, int force_split
   args.kb = K / tc::kGemmBK;
   const long long tiles = (long long)args.m_tiles * args.n_tiles;
   const int pairs = sms / 2;
+  // Residual epilogue (O / down, and the decode-only streaming scratch): every partial is a TMA
+  // bulk add, so the k-blocks are spread by GROUPED stream-K -- pair groups of n_tt siblings (one
+  // per token tile) walk the weight-tile-major (tile, k-block) stream in lockstep, group g taking
+  // [W g / G, W (g+1) / G) (W = weight tiles * kb), cut at tile boundaries. Every pair gets the same
+  // k-blocks whatever the tile count (O at T = 576: 16 weight tiles x 3 token tiles = 48 units on
+  // 74 pairs left a third of the pairs idle), and siblings read each weight k-block together, so
+  // it leaves DRAM once. TC_WS_STREAMK=0: k-split units instead (A/B).
+  static const int streamk_mode = [] {
+    const char* e = std::getenv("TC_WS_STREAMK");
+    return e ? std::atoi(e) : 1;
+  }();
   int sp = 1;
   if (epi == tc::EPI_RESID_F32) {
     if (force_splits > 0) {
       sp = force_splits;
     } else if (tiles < pairs) {
-      // red.add split-K: minimise waves * (k-blocks per split + per-unit overhead of ~8 k-blocks)
+      // k-split units: minimise waves * (k-blocks per split + per-unit overhead of ~8 k-blocks)
       double best = 1e30;
       for (int cand = 1; cand <= std::min(16, std::max(1, args.kb / 4)); ++cand) {
         const long long waves = (tiles * cand + pairs - 1) / pairs;
@@ -437,32 +404,17 @@ tc::GemmArgs plan_gemm_ws(int M, int N, int K, int epi, int sms, int force_split
   }
   args.splits = std::max(1, std::min(sp, args.kb));
   args.units = (int)(tiles * args.splits);
-  // residual epilogue (incl. the decode-only streaming scratch) with one token tile and more weight
-  // tiles than pairs (decode-only gate_up: 112 on 74): stream-K evens the k-blocks per pair
-  // (-5%). With several token tiles the tile-major stream would separate the sibling pairs that
-  // share a weight tile (its L2 reuse; down +15%), and with fewer tiles than pairs the k-split
-  // units already fill one wave. TC_WS_STREAMK=0 disables it, =2 forces it (A/B).
-  static const int streamk_mode = [] {
-    const char* e = std::getenv("TC_WS_STREAMK");
-    return e ? std::atoi(e) : 1;
-  }();
-  static const int ws_dbg = [] {
-    const char* e = std::getenv("TC_WS_DBG");
-    return e ? std::atoi(e) : 0;
-  }();
-  args.dbg = ws_dbg;
-  args.streamk = (epi == tc::EPI_RESID_F32 && force_splits == 0 &&
-                  (streamk_mode == 2 || (streamk_mode == 1 && n_tt == 1 && tiles > pairs))) ? 1 : 0;
+  args.streamk = (epi == tc::EPI_RESID_F32 && force_splits == 0 && streamk_mode != 0 && n_tt <= pairs) ? 1 : 0;
   if (args.streamk) {
     args.splits = 1;
-    args.units = (int)std::min<long long>(pairs, tiles * args.kb);  // one k-block range per pair
+    args.groups = (int)std::min<long long>(pairs / n_tt, (long long)args.n_tiles * args.kb);
+    args.units = args.groups * n_tt;  // pairs launched
   }
   return args;
 }
 
 int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi, int sms,
-                cudaStream_t s, int force_splits, const tc::QkvRopeArgs* rope, const CUtensorMap* out_map,
-                const NextGemm* next = nullptr) {
+                cudaStream_t s, int force_splits, const tc::QkvRopeArgs* rope, const CUtensorMap* out_map) {
   const int N = (int)w.rows;
   TC_REQUIRE(N % 256 == 0, "gemm_ws: weight rows must be a multiple of 256");
   const int pairs = sms / 2;
@@ -472,25 +424,6 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
   }();
   if (force_splits == 0 && env_splits > 0) force_splits = env_splits;
   tc::GemmArgs args = plan_gemm_ws(M, N, (int)w.cols, epi, sms, force_splits);
-  // off by default: measured -0.5% (mixed) / -1.7% (decode-only) -- the fill is not DRAM-bound
-  static const bool l2_next = [] {
-    const char* e = std::getenv("TC_WS_PF_NEXT");
-    return e && e[0] == '1';
-  }();
-  const CUtensorMap* next_map = &w.map(128);
-  if (l2_next && next && next->w && next->w->rows % 256 == 0) {
-    const tc::GemmArgs nx = plan_gemm_ws(next->M, (int)next->w->rows, (int)next->w->cols, next->epi, sms, 0);
-    args.nx_on = 1;
-    args.nx_m_tiles = nx.m_tiles;
-    args.nx_splits = nx.splits;
-    args.nx_kb = nx.kb;
-    args.nx_units = nx.units;
-    args.nx_streamk = nx.streamk;
-    args.nx_pairs = (int)std::min<long long>(pairs, nx.units);
-    args.nx_stages = nx.stages;
-    args.nx_total = nx.m_tiles * nx.n_tiles * nx.kb;
-    next_map = &next->w->map(128);
-  }
   args.out = out;
   args.ldo = ldo;
   args.bias = bias;
@@ -498,15 +431,6 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
     TC_REQUIRE(128 % rope->head_dim == 0, "gemm_ws: a 128-row half tile must cover whole heads");
     args.rope = *rope;
-    // off: measured slower (qkv 1.17 -> 1.55 ms per step): the 96 KB per CTA staging burst costs
-    // more than the per-chunk table loads it removes
-    static const bool rope_stage_on = [] {
-      const char* e = std::getenv("TC_WS_ROPE_SMEM");
-      return e && e[0] == '1';
-    }();
-    // every pair owns exactly one unit -> its ring is idle during the epilogue
-    args.rope_stage = rope_stage_on && args.units <= pairs && !args.streamk &&
-                      (size_t)args.tn * (rope->head_dim / 2) * 8 <= (size_t)args.stages * tc::ws_stage_bytes(args.tn);
   }
   const int grid = 2 * (int)std::min<long long>(pairs, args.units);
   // TC_WS_TRACE=1 (tools only): per-CTA %globaltimer timeline of this launch printed to stderr
@@ -523,8 +447,7 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     TC_REQUIRE(ldo == N, "gemm_ws: residual output must be dense [M, N]");
     resid_map = out_map ? *out_map : make_resid_map(out, (uint64_t)M, (uint64_t)N);
   }
-  launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), *next_map, args, epi,
-                 grid, s);
+  launch_gemm_ws(w.map(128), a.box(args.tn / 2), epi == tc::EPI_RESID_F32 ? resid_map : w.map(128), args, epi, grid, s);
   TC_CUDA(cudaGetLastError());
   if (trace) {
     std::vector<unsigned long long> h((size_t)grid * 16);
@@ -553,13 +476,12 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
 // out = epi(A[M,K] * W[N,K]^T). a: the activation buffer's maps.
 int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
              int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
-             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr, const CUtensorMap* out_map = nullptr,
-             const NextGemm* next = nullptr) {
+             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr, const CUtensorMap* out_map = nullptr) {
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(K % 64 == 0, "gemm: K must be a multiple of 64");
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
-  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256 || force_bn == 512 || force_bn == 1024,
-             "gemm: tile width must be 128, 256, 512 (= 2-SM 256 x 256) or 1024 (= weight-stationary pair)");
+  TC_REQUIRE(force_bn == 0 || force_bn == 128 || force_bn == 256 || force_bn == 1024,
+             "gemm: tile width must be 128, 256 or 1024 (= weight-stationary pair)");
   static const bool ws_small = [] {
     const char* e = std::getenv("TC_WS_SMALL");
     return !(e && e[0] == '0');
@@ -569,55 +491,11 @@ int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfl
     // streaming mode (decode-only steps): split-K partials land in the zeroed fp32 scratch via
     // TMA bulk adds; the finish kernel applies RoPE + KV append / SwiGLU
     if (red_out != nullptr) return run_gemm_ws(a, w, M, red_out, N, nullptr, tc::EPI_RESID_F32, sms, s, force_splits,
-                                               nullptr, nullptr, next);
-    return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map, next);
+                                               nullptr, nullptr);
+    return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map);
   }
   const CUtensorMap& a_map = a.m128;
-  const bool two_sm = N % 256 == 0 && (force_bn == 512 || (force_bn == 0 && M > kGemm2MinM));
-  if (two_sm) {
-    // pair tiles of 256 rows; splits only through red.add (residual / streaming epilogues)
-    tc::GemmArgs args{};
-    args.M = M;
-    args.N = N;
-    args.K = K;
-    args.m_tiles = (M + 255) / 256;
-    args.n_tiles = N / 256;
-    args.kb = K / tc::kGemmBK;
-    const long long tiles = (long long)args.m_tiles * args.n_tiles;
-    const int pairs = sms / 2;
-    int sp = 1;
-    if (force_splits > 0 && (epi == tc::EPI_RESID_F32 || red_out)) {
-      sp = force_splits;
-    } else if ((epi == tc::EPI_RESID_F32 || red_out) && tiles < pairs) {
-      double best = 1e30;
-      for (int cand = 1; cand <= std::min(16, std::max(1, args.kb / 4)); ++cand) {
-        const long long waves = (tiles * cand + pairs - 1) / pairs;
-        const double t = (double)waves * ((args.kb + cand - 1) / cand + 8);
-        if (t < best - 1e-9) {
-          best = t;
-          sp = cand;
-        }
-      }
-    }
-    args.splits = sp;
-    args.units = (int)(tiles * sp);
-    args.out = out;
-    args.ldo = ldo;
-    args.bias = bias;
-    args.ws = sk.ws;
-    args.tile_cnt = sk.cnt;
-    args.red_out = red_out;
-    if (epi == tc::EPI_QKV_ROPE && red_out == nullptr) {
-      TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
-      TC_REQUIRE(256 % rope->head_dim == 0, "gemm: tile width must cover whole heads");
-      args.rope = *rope;
-    }
-    const int grid = 2 * (int)std::min<long long>(pairs, args.units);
-    launch_gemm_2sm(a_map, w.map(128), args, epi, grid, s);
-    TC_CUDA(cudaGetLastError());
-    return 1;
-  }
-  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn == 512 ? 0 : force_bn, force_splits, red_out != nullptr);
+  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits, red_out != nullptr);
   TC_REQUIRE((long long)c.m_tiles * c.n_tiles <= kSkMaxTiles, "gemm: too many tiles");
   tc::GemmArgs args{};
   args.M = M;
@@ -1051,14 +929,6 @@ struct ProfScope {
   }
 };
 
-bool dec_2cta() {
-  static const bool on = [] {
-    const char* e = std::getenv("TC_DEC_2CTA");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 template <int DH, int G>
 void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int hk = I->d.n_kv_heads;
@@ -1066,11 +936,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     // decode on the main stream over sms - pf_sms CTAs (launched first, so its persistent CTAs
     // take their SMs), prefill beside it on stream_pf over whatever SMs remain; join before O
     TC_CUDA(cudaEventRecord(I->ev_fork, I->stream));
-    if (dec_2cta() && DH == 128)
-      launch_k(tc::attn_decode<DH, G, 96 * 1024>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G, 96 * 1024>::kBytes,
-               I->stream, I->kv_map, p);
-    else
-      launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
     TC_CUDA(cudaStreamWaitEvent(I->stream_pf, I->ev_fork, 0));
     launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
              I->kv2_map, I->q_map, p);
@@ -1081,20 +947,12 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     return;
   }
   if (n_qblk > 0) {
-#if TC_PREFILL_MMA_SYNC
-    tc::attn_prefill<DH, G><<<dim3(n_qblk, hk), tc::kPrefillThreads, tc::PrefillSmem<DH>::kBytes, I->stream>>>(I->kv_map, p);
-#else
     launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream,
              I->kv2_map, I->q_map, p);
-#endif
     ++I->launches;
   }
   if (n_dec > 0) {
-    if (dec_2cta() && DH == 128)
-      launch_k(tc::attn_decode<DH, G, 96 * 1024>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G, 96 * 1024>::kBytes,
-               I->stream, I->kv_map, p);
-    else
-      launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
     ++I->launches;
   }
   TC_CUDA(cudaGetLastError());
@@ -1145,11 +1003,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     if (EvPtr e = inbound_pending(I, st->decode[i].req_id)) waits.push_back(e);
 
   const int G = m.n_heads / m.n_kv_heads;
-#if TC_PREFILL_MMA_SYNC
-  const int tpc = 4 * (16 / G);  // prefill tokens per attention CTA
-#else
   const int tpc = 128 / G;  // prefill tokens per attention CTA (one 128-row q tile)
-#endif
   int n_qblk = 0, n_logit = 0, n_bt = 0;
   for (int i = 0; i < n_pf; ++i) {
     n_qblk += (st->prefill[i].n_tokens + tpc - 1) / tpc;
@@ -1181,8 +1035,14 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     // CTA-us: ~2.5 us per 128-key tile plus ~4 us fixed per CTA (Q load, TMEM, epilogue)
     const double w_pf = (2.5 * (double)pf_tiles + 4.0 * n_qblk * m.n_kv_heads) * (m.head_dim / 128.0);
     const double dec_bytes = (double)W * ps * m.head_dim * 2 * 2;
+    // decode page-stream rate per SM and its HBM cap (bytes per us); TC_DEC_RATE="per_sm,cap" (GB/s)
+    static const std::pair<double, double> dec_rate = [] {
+      double a = 40.0, b = 5200.0;
+      if (const char* e = std::getenv("TC_DEC_RATE")) std::sscanf(e, "%lf,%lf", &a, &b);
+      return std::make_pair(a * 1e3, b * 1e3);
+    }();
     auto t_of = [&](int P) {
-      const double t_dec = dec_bytes / std::min((I->sms - P) * 40e3, 5.2e6);  // us (bytes / (bytes per us))
+      const double t_dec = dec_bytes / std::min((I->sms - P) * dec_rate.first, dec_rate.second);  // us
       return t_dec + std::max(0.0, w_pf - P * t_dec) / I->sms;
     };
     const int p_max = std::min(n_qblk * m.n_kv_heads, I->sms / 2);
@@ -1202,8 +1062,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     I->pf_sms = std::max(0, std::min({want, n_qblk * m.n_kv_heads, I->sms / 2}));
   }
   const int dec_sms = I->sms - I->pf_sms;
-  const int dec_ctas = (dec_2cta() && m.head_dim == 128) ? 2 * dec_sms : dec_sms;
-  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_ctas, (W + 7) / 8)) : 0;
+  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_sms, (W + 7) / 8)) : 0;
   // entries: one per (CTA, segment overlap); at most n_seg + dec_grid
   const int max_entries = n_seg + dec_grid;
   // layout of the metadata block
@@ -1364,18 +1223,6 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   ap.ws_o = I->attn_ws_o;
   ap.dec_cnt = I->attn_cnt;
   ap.ws_ml = I->attn_ws_ml;
-  static const int pf_poly = [] {
-    const char* e = std::getenv("TC_PF_POLY");
-    return e ? std::atoi(e) : 0;
-  }();
-  ap.pf_poly = pf_poly;
-  // off: measured slower (decode-only attention 1.79 -> 2.10 ms/step); the extra requests
-  // contend with the page stream itself
-  static const int dec_l2 = [] {
-    const char* e = std::getenv("TC_DEC_L2");
-    return e ? std::atoi(e) : 0;
-  }();
-  ap.dec_l2_ahead = dec_l2;
   tc::QkvRopeArgs rp{};
   rp.kv = I->kv;
   rp.rope_cs = I->rope;
@@ -1393,14 +1240,6 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   // decode-heavy steps: QKV / gate_up stream their weights over every SM (split-K, red.add into a
   // zeroed fp32 scratch) and a finish kernel applies RoPE + KV append / SwiGLU
   const bool streaming = T <= kStreamRows;
-  // plan of the GEMM that follows (its weights' first k-blocks are prefetched into L2)
-  auto next_gemm = [&](const WMat* w, int epi_full) {
-    NextGemm n;
-    n.w = w;
-    n.M = T;
-    n.epi = streaming && (epi_full == tc::EPI_QKV_ROPE || epi_full == tc::EPI_SWIGLU) ? tc::EPI_RESID_F32 : epi_full;
-    return n;
-  };
   for (int l = 0; l < m.n_layers; ++l) {
     const LayerW& L = I->layers[l];
     {
@@ -1413,16 +1252,15 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       // QKV projection with fused bias, RoPE and paged KV append (q stays in I->qkv)
       ProfScope p_(I, "gemm_qkv");
       rp.layer = l;
-      const NextGemm nx_o = next_gemm(&L.o, tc::EPI_RESID_F32);
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.qkv, T, nullptr, I->qkv_n, nullptr, tc::EPI_BF16, I->sms, I->sk, s, 0, 0,
-                                nullptr, I->stream_scr, nullptr, &nx_o);
+                                nullptr, I->stream_scr, nullptr);
         launch_k(tc::finish_qkv_rope, dim3((I->qkv_n / 16 + 255) / 256, T), 256, 0, s, I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
                                                       I->qkv_n);
         ++I->launches;
       } else {
         I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
-                                tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp, nullptr, nullptr, &nx_o);
+                                tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp, nullptr, nullptr);
       }
     }
     {
@@ -1432,9 +1270,8 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_o");
-      const NextGemm nx_gu = next_gemm(&L.gate_up, tc::EPI_SWIGLU);
       I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
-                              nullptr, nullptr, &I->map_resid, &nx_gu);
+                              nullptr, nullptr, &I->map_resid);
     }
     {
       ProfScope p_(I, "norm");
@@ -1444,22 +1281,20 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     }
     {
       ProfScope p_(I, "gemm_gate_up");
-      const NextGemm nx_down = next_gemm(&L.down, tc::EPI_RESID_F32);
       if (streaming) {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, nullptr, m.ffn_dim, nullptr, tc::EPI_BF16, I->sms, I->sk, s,
-                                0, 0, nullptr, I->stream_scr, nullptr, &nx_down);
+                                0, 0, nullptr, I->stream_scr, nullptr);
         launch_k(tc::finish_swiglu, dim3((m.ffn_dim / 4 + 255) / 256, T), 256, 0, s, I->stream_scr, T, m.ffn_dim, I->act);
         ++I->launches;
       } else {
         I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s,
-                                0, 0, nullptr, nullptr, nullptr, &nx_down);
+                                0, 0, nullptr, nullptr, nullptr);
       }
     }
     {
       ProfScope p_(I, "gemm_down");
-      const NextGemm nx_qkv = l + 1 < m.n_layers ? next_gemm(&I->layers[l + 1].qkv, tc::EPI_QKV_ROPE) : NextGemm{};
       I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
-                              nullptr, nullptr, &I->map_resid, &nx_qkv);
+                              nullptr, nullptr, &I->map_resid);
     }
   }
   if (n_logit > 0) {

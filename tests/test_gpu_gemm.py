@@ -85,48 +85,6 @@ def test_gemm_f32_logits(cuda_ok, m, n, k):
     _close(out, a.float() @ b.float().T, False)
 
 
-# ---- 2-SM (CTA pair, tcgen05.mma.cta_group::2) variant, forced with bn=512
-@pytest.mark.parametrize("m,n,k", [(576, 6144, 4096), (1, 256, 128), (300, 512, 1024), (1100, 1024, 4096),
-                                   (256, 256, 64)])
-def test_gemm_2sm_bf16(cuda_ok, m, n, k):
-    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
-    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
-    out = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
-    _run(a, b, out, m, n, k, EPI_BF16, bn=512)
-    _close(out, a.float() @ b.float().T, True)
-
-
-@pytest.mark.parametrize("m,n,k,splits", [(576, 4096, 14336, 0), (576, 4096, 4096, 3), (64, 4096, 4096, 0)])
-def test_gemm_2sm_residual(cuda_ok, m, n, k, splits):
-    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
-    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.02
-    resid = torch.randn(m, n, device="cuda", dtype=torch.float32)
-    ref = resid + a.float() @ b.float().T
-    _run(a, b, resid, m, n, k, EPI_RESID, bn=512, splits=splits)
-    _close(resid, ref, False)
-
-
-def test_gemm_2sm_swiglu_bias_f32(cuda_ok):
-    m, f, k = 576, 14336, 4096
-    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
-    wg = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
-    wu = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
-    phys = torch.stack([wg.view(f // 64, 64, k), wu.view(f // 64, 64, k)], dim=1).reshape(2 * f, k).contiguous()
-    out = torch.zeros(m, f, device="cuda", dtype=torch.bfloat16)
-    _run(a, phys, out, m, 2 * f, k, EPI_SWIGLU, bn=512)
-    _close(out, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T), True)
-    n = 7168
-    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.05
-    bias = torch.randn(n, device="cuda", dtype=torch.bfloat16)
-    o2 = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
-    _run(a, b, o2, m, n, k, EPI_BIAS, bias=bias, bn=512)
-    _close(o2, a.float() @ b.float().T + bias.float(), True)
-    o3 = torch.zeros(65, 128256 // 4 * 4, device="cuda", dtype=torch.float32)
-    b3 = torch.randn(128256, k, device="cuda", dtype=torch.bfloat16) * 0.03
-    _run(a[:65].contiguous(), b3, o3, 65, 128256, k, EPI_F32, bn=512)
-    _close(o3, a[:65].float() @ b3.float().T, False)
-
-
 # ---- weight-stationary pair variant (gemm_ws.cuh: tokens on the MMA's N), forced with bn=1024;
 # the token tile TN = round_up(T / ceil(T / 256), 32) covers ragged T (1, 20, 100, 300, 1100 ...)
 @pytest.mark.parametrize("m,n,k", [(576, 6144, 4096), (1, 256, 128), (20, 512, 256), (100, 512, 1024),
@@ -141,11 +99,14 @@ def test_gemm_ws_bf16(cuda_ok, m, n, k):
     _close(out, a.float() @ b.float().T, True)
 
 
-# (64, 28672, ...) and (200, 20480, ...): one token tile, more weight tiles than CTA pairs -> the
-# stream-K partition (each pair a contiguous k-block range across tile boundaries)
+# splits = 0: grouped stream-K (pair groups of one pair per token tile walk the weight-tile-major
+# k-block stream; ranges cut across tile boundaries): one token tile with more weight tiles than
+# pairs (64 x 28672, 200 x 20480), several token tiles (576 -> 3, 1100 -> 5, 3000 -> 12 tiles:
+# 6 groups), fewer k-blocks than groups (7 x 256 x 128).
 @pytest.mark.parametrize("m,n,k,splits", [(576, 4096, 14336, 0), (576, 4096, 4096, 3), (576, 4096, 4096, 1),
                                           (64, 4096, 4096, 0), (333, 5120, 13824, 0), (7, 256, 512, 2),
-                                          (64, 28672, 1024, 0), (200, 20480, 704, 0)])
+                                          (64, 28672, 1024, 0), (200, 20480, 704, 0), (576, 4096, 4096, 0),
+                                          (1100, 4096, 4096, 0), (3000, 512, 1024, 0), (7, 256, 128, 0)])
 def test_gemm_ws_residual(cuda_ok, m, n, k, splits):
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16) * 0.02
