@@ -430,39 +430,41 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 // [W*c/NC, W*(c+1)/NC), so every SM streams the same number of bytes whatever the context
 // mix. A CTA's range is a list of ENTRIES (segment, page0, page1, part).
 //
-// Inside a CTA: one producer warp walks the entries and streams each page's K and V blocks
-// (one TMA box, 8 KiB at head_dim 128) into the ring, plus the segment's q rows (one bulk
-// copy per entry) into a double-buffered q slot; it never waits for a consumer except on a
-// full ring. Consumer warp w takes ring stages w, w+NC, w+2NC, ... and keeps its own online-
-// softmax state per entry; at the end of an entry the NC partial states meet in shared memory
-// (one named barrier) and warp (entry % NC) merges them. Only segments cut by a CTA boundary
-// (at most 2 per CTA) go through global memory: the merging warp writes its partial, and the
-// CTA that arrives last on the segment's counter combines the parts.
-//
-// The consumers, not the ring, set the page rate (round 1: 4 warps at ~1,200 cycles per page
-// each = ~40 GB/s per SM, a quarter of the samples waiting on a full barrier): 8 consumer warps
-// over a 128 KiB ring, and a page costs ~110 instructions -- 16 + 16 mma.sync, 16 ldmatrix, the
-// key mask only on a segment's last page, and a lazy softmax base (the base, and with it l and o,
-// moves only when a row's max grows by more than 2^8, which after the first page is rare).
-constexpr int kDecConsumers = 8;
-constexpr int kDecThreads = (kDecConsumers + 1) * 32;
-constexpr int kDecRingBytes = 128 * 1024;
+// Warp roles inside a CTA:
+//   consumers (NC warps)  warp w takes ring stages w, w+NC, ... of the page stream and keeps its
+//                         own online-softmax state per entry; at the end of an entry it publishes
+//                         the state into the entry's partial buffer (double-buffered, mbarriers)
+//                         and goes straight on to the next entry's pages.
+//   producer              streams each page's K and V blocks (one TMA box, 8 KiB at head_dim
+//                         128) into the ring and the segment's q rows (one bulk copy per entry)
+//                         into a double-buffered q slot; it waits only on a full ring.
+//   merger                combines the NC partial states of each entry and writes the output
+//                         row; only segments cut by a CTA boundary (at most 2 per CTA) go through
+//                         global memory (the CTA that arrives last on the segment's counter
+//                         combines the parts).
+// Round 1 merged in a consumer warp behind a consumer-wide barrier: the ring stages owned by the
+// merging warp stalled the in-order producer at every entry boundary.
+// A page costs a consumer ~110 instructions: 16 + 16 mma.sync, 16 ldmatrix, the key mask only on
+// a segment's last page, and a lazy softmax base (the base -- and with it l and o -- moves only
+// when a row's max grows by more than 2^8, which after the first page is rare).
+constexpr int kDecRingBytes = 192 * 1024;
 constexpr float kDecRescaleLog2 = 8.f;  // lazy base: p = 2^(s - base) <= 2^8, P stays in bf16 range
+__host__ __device__ constexpr int dec_threads(int nc) { return (nc + 2) * 32; }
 
-template <int DH, int G>
+template <int DH, int G, int NC>
 struct DecodeSmem {
   static constexpr int kStageBytes = KvBlock<DH>::kPairBytes;  // one page-head: K block then V block
   static constexpr int kStages = kDecRingBytes / kStageBytes;
   static constexpr int kQBytes = G * DH * 2;
-  static constexpr int kPartFloats = kDecConsumers * G * DH;  // per buffer
+  static constexpr int kPartFloats = NC * G * DH;  // per buffer
   static constexpr int kOffQ = kDecRingBytes;
   static constexpr int kOffPart = kOffQ + 2 * ((kQBytes + 127) / 128 * 128);
   static constexpr int kOffMl = kOffPart + 2 * kPartFloats * 4;
-  static constexpr int kBytes = kOffMl + 2 * kDecConsumers * G * 2 * 4 + 1024;
+  static constexpr int kBytes = kOffMl + 2 * NC * G * 2 * 4 + 1024;
   // Stage g is consumed by warp g % NC. With S a multiple of NC every slot has ONE owner warp,
   // which waits for use k+1 only after finishing use k; otherwise a warp running a lap ahead
   // could pass a parity wait on a phase that has not landed yet (mbarrier parity ABA).
-  static_assert(kStages % kDecConsumers == 0, "decode ring: stages must be a multiple of the consumer warps");
+  static_assert(kStages % NC == 0, "decode ring: stages must be a multiple of the consumer warps");
   static_assert(kBytes <= 227 * 1024, "decode smem");
 };
 
@@ -471,7 +473,6 @@ TC_DEVICE void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-TC_DEVICE void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kDecConsumers * 32) : "memory"); }
 
 // Merge n partial states (m, l in the log2 domain; o unnormalised) for G rows; lane handles
 // dims lane*V .. lane*V+V-1. load_ml(j, r) -> float2(m, l); load_o(j, r, dst[V]).
@@ -571,14 +572,13 @@ TC_DEVICE void dec_page(const uint32_t (&qf)[DH / 16][4], uint32_t kv_smem, int 
   attn_pv<DH, 2>(s, kv_smem, 0, o);
 }
 
-template <int DH, int G>
-__global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  using SM = DecodeSmem<DH, G>;
+template <int DH, int G, int NC>
+__global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  using SM = DecodeSmem<DH, G, NC>;
   constexpr int S = SM::kStages;
-  constexpr int NC = kDecConsumers;
   constexpr int V = DH / 32;
   extern __shared__ uint8_t attn_smem_raw[];
-  __shared__ uint64_t full[S], empty[S], qfull[2], qempty[2];
+  __shared__ uint64_t full[S], empty[S], qfull[2], qempty[2], pfull[2], pempty[2];
   const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
   uint8_t* gbase = attn_smem_raw + (sbase - smem_u32(attn_smem_raw));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -591,6 +591,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_const
     for (int b = 0; b < 2; ++b) {
       mbar_init(&qfull[b], 1);
       mbar_init(&qempty[b], NC);
+      mbar_init(&pfull[b], NC);
+      mbar_init(&pempty[b], 1);
     }
     mbar_fence_init();
   }
@@ -598,6 +600,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_const
   pdl_wait();  // q / K / V written by the QKV GEMM (dec_cta_off above came from a memcpy)
   pdl_trigger();
   const int qkv_ld = (p.n_heads + 2 * p.n_kv_heads) * DH;
+  float* part_o = reinterpret_cast<float*>(gbase + SM::kOffPart);
+  float* part_ml = reinterpret_cast<float*>(gbase + SM::kOffMl);
 
   if (warp == NC) {
     // ------------------------------------------------------------ producer
@@ -642,29 +646,96 @@ __global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_const
     return;
   }
 
+  if (warp == NC + 1) {
+    // ------------------------------------------------------------ merger
+    for (int e0 = e_begin; e0 < e_end; e0 += 32) {
+      int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0), sb = make_int4(0, 0, 0, 0);
+      if (e0 + lane < e_end) {
+        ent = p.dec_entries[e0 + lane];
+        sa = p.dec_seg_a[ent.x];
+        sb = p.dec_seg_b[ent.x];
+      }
+      const int ne = min(32, e_end - e0);
+      for (int k = 0; k < ne; ++k) {
+        const int e = e0 + k - e_begin;
+        const int seg = __shfl_sync(0xffffffffu, ent.x, k), part = __shfl_sync(0xffffffffu, ent.w, k);
+        const int q_row = __shfl_sync(0xffffffffu, sa.z, k), kvh = __shfl_sync(0xffffffffu, sa.w, k);
+        const int n_parts = __shfl_sync(0xffffffffu, sb.x, k), ws_base = __shfl_sync(0xffffffffu, sb.y, k);
+        const int b = e & 1;
+        mbar_wait(&pfull[b], (e >> 1) & 1);
+        const float* bo = part_o + (b * NC * G) * DH;
+        const float* bml = part_ml + (b * NC * G) * 2;
+        float acc[G][V], mm[G], ll[G];
+        merge_partials<DH, G>(
+            NC, [&](int j, int r) { return *reinterpret_cast<const float2*>(bml + (j * G + r) * 2); },
+            [&](int j, int r, float* d) {
+              const float* src = bo + (j * G + r) * DH + lane * V;
+#pragma unroll
+              for (int x = 0; x < V; ++x) d[x] = src[x];
+            },
+            acc, mm, ll);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[b]);  // buffer b free for entry e + 2
+        __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
+        if (n_parts == 1) {
+          store_out_row<DH, G>(out_row, acc, ll);
+          continue;
+        }
+        // segment cut by a CTA boundary: publish the CTA's part; the last arriver combines
+        const int slot = ws_base + part;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+          float* dst = p.ws_o + ((long long)slot * G + r) * DH + lane * V;
+#pragma unroll
+          for (int x = 0; x < V; ++x) dst[x] = acc[r][x];
+          if (lane == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)slot * G + r) * 2) = make_float2(mm[r], ll[r]);
+        }
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          __threadfence();
+          int* cnt = p.dec_cnt + seg;
+          last = atomicAdd(cnt, 1) == n_parts - 1;
+          if (last) *cnt = 0;  // ready for the next layer / step
+        }
+        if (!__shfl_sync(0xffffffffu, last, 0)) continue;
+        __threadfence();
+        merge_partials<DH, G>(
+            n_parts,
+            [&](int j, int r) { return __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(ws_base + j) * G + r) * 2)); },
+            [&](int j, int r, float* d) {
+              const float* src = p.ws_o + ((long long)(ws_base + j) * G + r) * DH + lane * V;
+              if constexpr (V == 4) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+                d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+              } else {
+                const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+                d[0] = t.x; d[1] = t.y;
+              }
+            },
+            acc, mm, ll);
+        store_out_row<DH, G>(out_row, acc, ll);
+      }
+    }
+    return;
+  }
+
   // -------------------------------------------------------------- consumers
   const int r_lo = lane / 4;
   const bool ok_lo = r_lo < G;
   const int c0 = (lane % 4) * 2;
-  float* part_o = reinterpret_cast<float*>(gbase + SM::kOffPart);
-  float* part_ml = reinterpret_cast<float*>(gbase + SM::kOffMl);
   int g_base = 0;  // stages before the current entry
   for (int e0 = e_begin; e0 < e_end; e0 += 32) {
-    int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0), sb = make_int4(0, 0, 0, 0);
+    int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0);
     if (e0 + lane < e_end) {
       ent = p.dec_entries[e0 + lane];
       sa = p.dec_seg_a[ent.x];
-      sb = p.dec_seg_b[ent.x];
     }
     const int ne = min(32, e_end - e0);
     for (int k = 0; k < ne; ++k) {
       const int e = e0 + k - e_begin;
-      const int seg = __shfl_sync(0xffffffffu, ent.x, k);
       const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
-      const int part = __shfl_sync(0xffffffffu, ent.w, k);
-      const int kv_len = __shfl_sync(0xffffffffu, sa.y, k), q_row = __shfl_sync(0xffffffffu, sa.z, k);
-      const int kvh = __shfl_sync(0xffffffffu, sa.w, k);
-      const int n_parts = __shfl_sync(0xffffffffu, sb.x, k), ws_base = __shfl_sync(0xffffffffu, sb.y, k);
+      const int kv_len = __shfl_sync(0xffffffffu, sa.y, k);
       const int b = e & 1;
       // q fragment (rows >= G are zero) from the entry's q slot
       uint32_t qf[DH / 16][4];
@@ -700,6 +771,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_const
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], 1);
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], 2);
       // publish this warp's partial state (a warp without pages publishes m = -inf, l = 0, o = 0)
+      mbar_wait(&pempty[b], ((e >> 1) & 1) ^ 1);  // the merger is done with entry e - 2
       float* po = part_o + ((b * NC + warp) * G) * DH;
       float* pml = part_ml + ((b * NC + warp) * G) * 2;
       if (ok_lo) {
@@ -707,59 +779,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) attn_decode(const __grid_const
         for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(po + r_lo * DH + c * 8 + c0) = make_float2(o[c][0], o[c][1]);
         if (lane % 4 == 0) *reinterpret_cast<float2*>(pml + r_lo * 2) = make_float2(m[0], l[0]);
       }
-      consumer_bar();
-      if (warp != e % NC) continue;
-      // merging warp: combine the NC warps' states of this entry
-      const float* bo = part_o + (b * NC * G) * DH;
-      const float* bml = part_ml + (b * NC * G) * 2;
-      float acc[G][V], mm[G], ll[G];
-      merge_partials<DH, G>(
-          NC, [&](int j, int r) { return *reinterpret_cast<const float2*>(bml + (j * G + r) * 2); },
-          [&](int j, int r, float* d) {
-            const float* src = bo + (j * G + r) * DH + lane * V;
-#pragma unroll
-            for (int x = 0; x < V; ++x) d[x] = src[x];
-          },
-          acc, mm, ll);
-      __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
-      if (n_parts == 1) {
-        store_out_row<DH, G>(out_row, acc, ll);
-        continue;
-      }
-      // segment cut by a CTA boundary: publish the CTA's part; the last arriver combines
-      const int slot = ws_base + part;
-#pragma unroll
-      for (int r = 0; r < G; ++r) {
-        float* dst = p.ws_o + ((long long)slot * G + r) * DH + lane * V;
-#pragma unroll
-        for (int x = 0; x < V; ++x) dst[x] = acc[r][x];
-        if (lane == 0) *reinterpret_cast<float2*>(p.ws_ml + ((long long)slot * G + r) * 2) = make_float2(mm[r], ll[r]);
-      }
       __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        __threadfence();
-        int* cnt = p.dec_cnt + seg;
-        last = atomicAdd(cnt, 1) == n_parts - 1;
-        if (last) *cnt = 0;  // ready for the next layer / step
-      }
-      if (!__shfl_sync(0xffffffffu, last, 0)) continue;
-      __threadfence();
-      merge_partials<DH, G>(
-          n_parts,
-          [&](int j, int r) { return __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((long long)(ws_base + j) * G + r) * 2)); },
-          [&](int j, int r, float* d) {
-            const float* src = p.ws_o + ((long long)(ws_base + j) * G + r) * DH + lane * V;
-            if constexpr (V == 4) {
-              const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
-              d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
-            } else {
-              const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
-              d[0] = t.x; d[1] = t.y;
-            }
-          },
-          acc, mm, ll);
-      store_out_row<DH, G>(out_row, acc, ll);
+      if (lane == 0) mbar_arrive(&pfull[b]);  // release: the partial's stores precede the arrival
     }
   }
 }

@@ -197,9 +197,12 @@ void init_kernel_attrs(int dev) {
   attr((const void*)tc::attn_prefill_tc<64, 2>, tc::PfCfg<64, 2>::kBytes);
   attr((const void*)tc::attn_prefill_tc<128, 4>, tc::PfCfg<128, 4>::kBytes);
   attr((const void*)tc::attn_prefill_tc<128, 5>, tc::PfCfg<128, 5>::kBytes);
-  attr((const void*)tc::attn_decode<64, 2>, tc::DecodeSmem<64, 2>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4>, tc::DecodeSmem<128, 4>::kBytes);
-  attr((const void*)tc::attn_decode<128, 5>, tc::DecodeSmem<128, 5>::kBytes);
+  attr((const void*)tc::attn_decode<64, 2, 4>, tc::DecodeSmem<64, 2, 4>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 4>, tc::DecodeSmem<128, 4, 4>::kBytes);
+  attr((const void*)tc::attn_decode<128, 5, 4>, tc::DecodeSmem<128, 5, 4>::kBytes);
+  attr((const void*)tc::attn_decode<64, 2, 6>, tc::DecodeSmem<64, 2, 6>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 6>, tc::DecodeSmem<128, 4, 6>::kBytes);
+  attr((const void*)tc::attn_decode<128, 5, 6>, tc::DecodeSmem<128, 5, 6>::kBytes);
   done.insert(dev);
 }
 
@@ -929,6 +932,23 @@ struct ProfScope {
   }
 };
 
+// decode attention consumer warps (TC_DEC_NC=4|6, A/B)
+int dec_nc() {
+  static const int nc = [] {
+    const char* e = std::getenv("TC_DEC_NC");
+    return e && std::atoi(e) == 6 ? 6 : 4;
+  }();
+  return nc;
+}
+
+template <int DH, int G>
+void launch_decode(tc_instance* I, const tc::AttnParams& p, int dec_grid) {
+  if (dec_nc() == 6)
+    launch_k(tc::attn_decode<DH, G, 6>, dec_grid, tc::dec_threads(6), tc::DecodeSmem<DH, G, 6>::kBytes, I->stream, I->kv_map, p);
+  else
+    launch_k(tc::attn_decode<DH, G, 4>, dec_grid, tc::dec_threads(4), tc::DecodeSmem<DH, G, 4>::kBytes, I->stream, I->kv_map, p);
+}
+
 template <int DH, int G>
 void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
   const int hk = I->d.n_kv_heads;
@@ -936,7 +956,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     // decode on the main stream over sms - pf_sms CTAs (launched first, so its persistent CTAs
     // take their SMs), prefill beside it on stream_pf over whatever SMs remain; join before O
     TC_CUDA(cudaEventRecord(I->ev_fork, I->stream));
-    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    launch_decode<DH, G>(I, p, dec_grid);
     TC_CUDA(cudaStreamWaitEvent(I->stream_pf, I->ev_fork, 0));
     launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
              I->kv2_map, I->q_map, p);
@@ -952,7 +972,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     ++I->launches;
   }
   if (n_dec > 0) {
-    launch_k(tc::attn_decode<DH, G>, dec_grid, tc::kDecThreads, tc::DecodeSmem<DH, G>::kBytes, I->stream, I->kv_map, p);
+    launch_decode<DH, G>(I, p, dec_grid);
     ++I->launches;
   }
   TC_CUDA(cudaGetLastError());
