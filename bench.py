@@ -34,6 +34,15 @@ REPO = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 
+# GPU-vs-oracle parity tests that run the exact step a bench line measures (layer-reduced model,
+# same shapes, same concurrent prefill/decode attention split)
+PARITY = {
+    ("llama3_8b", 512, 512, 64, 1024): "tests/test_gpu_bench_shapes.py::test_config2_bench_step_llama_shape",
+    ("qwen2_5_14b", 1024, 4096, 32, 8192): "tests/test_gpu_bench_shapes.py::test_config5_bench_step_qwen_shape",
+    ("llama3_8b", 0, 0, 64, 1024): "tests/test_gpu_bench_shapes.py::test_config2_bench_step_llama_shape (its decode rows)",
+}
+
+
 def step_cost(d, P, prefix, D, ctx, n_logit):
     """Algorithmic flops / bytes per kernel class for one step."""
     H, Hk, dh, dm, F, V, L = d["n_heads"], d["n_kv_heads"], d["head_dim"], d["d_model"], d["ffn_dim"], d["vocab"], d["n_layers"]
@@ -117,6 +126,44 @@ def cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=3):
             "seconds_per_step": sec, **det}
 
 
+def scheduler_baseline(config="configs/c3_llama8b_4p4d.json", repeat=5):
+    """the reference scheduler/engine on the host cores, single-threaded, on the
+    config-3 trace (4P1024 + 4D256, short_chat, 2000 requests) -- oracle/_ref/pdsim_oracle is the
+    reference's own pdsim headers compiled here (oracle/Makefile) -- next to this repo's drop-in
+    host engine (lib/taichi_sim), which makes the identical decisions (tests/test_engine_parity.py)."""
+    import platform
+    out = {"config": config, "threads": 1, "repeat": repeat, "cpu": platform.processor() or None,
+           "nproc": os.cpu_count()}
+    try:
+        out["cpu"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    for name, exe in (("reference", REPO / "oracle" / "_ref" / "pdsim_oracle"),
+                      ("ours", REPO / "paper_2508_01989_b200" / "lib" / "taichi_sim")):
+        if not exe.exists():
+            out[name] = {"unavailable": f"{exe.relative_to(REPO)} not built"}
+            continue
+        r = subprocess.run([str(exe), "bench", "--config", str(REPO / config), "--repeat", str(repeat)],
+                           capture_output=True, text=True, timeout=300)
+        out[name] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-300:]}
+    return out
+
+
+def memcpy_baseline(nbytes=512 << 20, reps=5):
+    """BASELINE.md 3.3 (context for the migration leg): a host memcpy of one 4096-token Llama-3-8B
+    request's KV (512 MiB), single thread, median of reps."""
+    import numpy as np
+    a = np.ones(nbytes, dtype=np.uint8)
+    b = np.empty_like(a)
+    ts = []
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        np.copyto(b, a)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts[1:])
+    return {"bytes": nbytes, "ms": t * 1e3, "gb_s": nbytes / t / 1e9, "threads": 1}
+
+
 def migration_bench(src, model, dev, hbm_gbs, n_tokens=(1024, 4096), reps=8):
     """KV migration: tc_kv_migrate of a request's first n_tokens rows
     between two instances, timed by the library with CUDA events around the page-copy kernel.
@@ -145,6 +192,64 @@ def migration_bench(src, model, dev, hbm_gbs, n_tokens=(1024, 4096), reps=8):
     return {"kernel": "kv_copy_pages (whole 2 MiB pages, 16 B vectors)", "path": "same-GPU pool-to-pool copy "
             "(1-GPU box): bound = HBM read+write; cross-GPU it is an NVLink P2P push (target 900 GB/s, not "
             "measurable on one GPU)", "median_of": reps, "sizes": out}
+
+
+def migration_nvlink(inst, rank, world, dev, n_tokens=4096, reps=8):
+    """KV migration across GPUs (K11 over NVLink), one process per GPU: rank 2k
+    (a prefill-heavy instance) pushes a 4096-token request's pages into rank 2k+1's pool (its
+    decode-heavy partner) through a CUDA IPC mapping (tc_kv_push_pages), all pairs at once after a
+    barrier. Device time per copy from CUDA events on the source's copy stream; GB/s vs 900."""
+    import torch.distributed as dist
+    from paper_2508_01989_b200 import RemotePool
+    rid = (1 << 41) + rank
+    info, res = None, None
+    try:
+        if rank % 2 == 1:
+            inst.kv_reserve(rid, n_tokens)
+            info = (inst.export_pool(), [int(x) for x in inst.kv_pages(rid)])
+    except Exception as e:  # noqa: BLE001 -- reported in the line, the step numbers stand
+        info = ("error", repr(e))
+    infos = [None] * world
+    dist.all_gather_object(infos, info)
+    remote = None
+    if rank % 2 == 0 and rank + 1 < world:
+        try:
+            peer = infos[rank + 1]
+            if peer[0] == "error":
+                raise RuntimeError(peer[1])
+            exported, dpages = peer
+            inst.kv_reserve(rid, n_tokens)
+            spages = [int(x) for x in inst.kv_pages(rid)]
+            remote = RemotePool(exported, device=dev)
+            ms, nbytes = [], 0
+            for i in range(reps + 2):
+                ev = inst.push_pages(remote, spages, dpages[:len(spages)])
+                t, nbytes = ev.wait()
+                ev.close()
+                if i >= 2:
+                    ms.append(t)
+            t = statistics.median(ms)
+            res = {"src": rank, "dst": rank + 1, "bytes": nbytes, "ms": t, "gb_s": nbytes / t / 1e6,
+                   "nvlink_frac": nbytes / t / 1e6 / 900.0}
+        except Exception as e:  # noqa: BLE001
+            res = {"src": rank, "dst": rank + 1, "error": repr(e)}
+    dist.barrier()
+    if remote is not None:
+        remote.close()
+    for r in (rid,):
+        try:
+            inst.kv_release(r)
+        except Exception:  # noqa: BLE001 -- not reserved on this rank
+            pass
+    out = [None] * world
+    dist.all_gather_object(out, res)
+    pairs = [r for r in out if r]
+    ok = [r for r in pairs if "gb_s" in r]
+    return {"kernel": "kv_migrate_pages via tc_kv_push_pages (CUDA IPC mapping of the peer's pool, NVLink P2P stores)",
+            "tokens": n_tokens, "median_of": reps, "pairs": pairs,
+            "min_pair_gb_s": min((r["gb_s"] for r in ok), default=None),
+            "min_nvlink_frac": min((r["nvlink_frac"] for r in ok), default=None),
+            "peak": "900 GB/s per direction per GPU (NVLink 5, nominal)"}
 
 
 def reduce_max(vals, device=None):
@@ -214,7 +319,7 @@ def main():
                 f"chunk size 512, single aggregated instance per GPU")
     config = {"workload": workload, "model_shape": args.model, "step_rows": P + D, "prefill_tokens": P,
               "prefill_prefix": prefix, "decode_reqs": D, "decode_ctx": ctx, "instances": world,
-              "l2": "inputs larger than L2 (15 GB weights + 8.6 GB KV per step), no flush needed"}
+              "l2": None}
     metric = "hybrid-step tokens/s"
 
     if args.impl == "reference":
@@ -256,6 +361,11 @@ def main():
     inst = Instance(args.model, device=dev, weight_seed=1, kv_pool_tokens=(D + 2) * (ctx + 64) + prefix + P + 8192,
                     max_step_tokens=max(P + D, 512), max_seqs=D + 8, max_context=max(ctx, prefix + P, 4096) + 64)
     dims = inst.dims.as_dict()
+    H_, Hk_, dh_, dm_, F_ = dims["n_heads"], dims["n_kv_heads"], dims["head_dim"], dims["d_model"], dims["ffn_dim"]
+    w_gb = 2 * (dims["n_layers"] * ((H_ + 2 * Hk_) * dh_ * dm_ + dm_ * H_ * dh_ + 3 * F_ * dm_) + 2 * dims["vocab"] * dm_) / 1e9
+    kv_gb = (D * (ctx + 1) + prefix + P) * 2 * dims["n_kv_heads"] * dims["head_dim"] * 2 * dims["n_layers"] / 1e9
+    config["l2"] = (f"inputs larger than L2 ({w_gb:.1f} GB weights + {kv_gb:.1f} GB KV read per step vs 126 MB L2), "
+                    f"no flush needed")
     V = dims["vocab"]
     import numpy as np
     rng = np.random.default_rng(1000 + rank)
@@ -327,7 +437,8 @@ def main():
     traffic = None
     tf = REPO / "profiles" / "gemm_gate_up_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        # per model shape: only an ncu capture of THIS model's gate_up launch counts as its traffic
+        traffic = json.loads(tf.read_text()).get(args.model, {}).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "kernel": "gemm_gate_up (tcgen05, fused SwiGLU)", "achieved": achieved,
                 "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus, "traffic": traffic,
                 "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
@@ -343,6 +454,8 @@ def main():
                                      "measured_ms": phases.get(k)} for k, v in cost.items()}}
 
     migration = migration_bench(inst, args.model, dev, hbm)
+    if world > 1:
+        migration["cross_gpu"] = migration_nvlink(inst, rank, world, dev)
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -358,7 +471,10 @@ def main():
                                      "weight_stream_bound_ms": 1e3 * sum(c["bytes"] for k, c in
                                                                          step_cost(dims, 0, 0, D, ctx, D).items()) /
                                                                (measured_peaks()[0] * 1e9)},
-                "migration": migration, "cpu_baseline": cb}
+                "migration": migration, "cpu_baseline": cb,
+                "parity": PARITY.get((args.model, P, prefix, D, ctx), "tests/test_gpu_step.py (shape-generic step parity)")}
+        if cb is not None:
+            line["cpu_baselines_extra"] = {"scheduler": scheduler_baseline(), "migration_memcpy": memcpy_baseline()}
         print(json.dumps(line))
     inst.close()
     if world > 1:

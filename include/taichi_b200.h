@@ -156,6 +156,25 @@ tc_status tc_kv_migrate_wait(tc_instance* src, float* copy_ms, int64_t* bytes);
 /* Grid of the copy kernel (0 = 2 x SMs, full bandwidth; fewer CTAs leave SMs to the steps). */
 tc_status tc_set_migration_ctas(tc_instance* inst, int32_t ctas);
 
+/* Cross-process KV migration (one process per GPU, the deployment bench.py --gpus N uses).
+ * The destination process exports its KV pool (CUDA IPC handle, TC_IPC_HANDLE_BYTES opaque bytes)
+ * and reserves pages for the request (tc_kv_reserve + tc_kv_pages); the source process imports the
+ * pool once and pushes pages with tc_kv_push_pages: the same copy kernel as tc_kv_migrate_async,
+ * on src's copy stream after its in-flight step, its stores going over NVLink to the peer GPU.
+ * Page bookkeeping stays with each owner: the destination's page list travels with the control
+ * message (the reference engine's Migration record, engine.hpp:388-413), the source releases its
+ * pages (tc_kv_release) once the event completed. Same-GPU imports (two processes on one GPU)
+ * work too; they are what the single-GPU tests exercise. */
+#define TC_IPC_HANDLE_BYTES 64
+typedef struct tc_remote_pool tc_remote_pool;
+tc_status tc_kv_pool_export(tc_instance* inst, void* handle /* TC_IPC_HANDLE_BYTES */, int64_t* page_bytes,
+                            int64_t* n_pages);
+tc_status tc_kv_pool_import(int32_t device, const void* handle, int64_t page_bytes, int64_t n_pages,
+                            tc_remote_pool** out);
+tc_status tc_remote_pool_close(tc_remote_pool* pool);
+tc_status tc_kv_push_pages(tc_instance* src, tc_remote_pool* dst, const int32_t* src_pages, const int32_t* dst_pages,
+                           int32_t n_pages, tc_event** ev);
+
 /* Device pointer of the KV pool and its geometry (tests / tools). */
 tc_status tc_kv_pool_info(tc_instance* inst, void** base, int64_t* page_bytes, int64_t* n_pages);
 /* Page list of req_id (caller buffer of capacity max_pages). */

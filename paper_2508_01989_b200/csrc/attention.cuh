@@ -447,17 +447,17 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 // A page costs a consumer ~110 instructions: 16 + 16 mma.sync, 16 ldmatrix, the key mask only on
 // a segment's last page, and a lazy softmax base (the base -- and with it l and o -- moves only
 // when a row's max grows by more than 2^8, which after the first page is rare).
-constexpr int kDecRingBytes = 192 * 1024;
+constexpr int kDecRingBytes = 192 * 1024;  // default ring (RING template parameter: A/B)
 constexpr float kDecRescaleLog2 = 8.f;  // lazy base: p = 2^(s - base) <= 2^8, P stays in bf16 range
 __host__ __device__ constexpr int dec_threads(int nc) { return (nc + 2) * 32; }
 
-template <int DH, int G, int NC>
+template <int DH, int G, int NC, int RING = kDecRingBytes>
 struct DecodeSmem {
   static constexpr int kStageBytes = KvBlock<DH>::kPairBytes;  // one page-head: K block then V block
-  static constexpr int kStages = kDecRingBytes / kStageBytes;
+  static constexpr int kStages = RING / kStageBytes;
   static constexpr int kQBytes = G * DH * 2;
   static constexpr int kPartFloats = NC * G * DH;  // per buffer
-  static constexpr int kOffQ = kDecRingBytes;
+  static constexpr int kOffQ = RING;
   static constexpr int kOffPart = kOffQ + 2 * ((kQBytes + 127) / 128 * 128);
   static constexpr int kOffMl = kOffPart + 2 * kPartFloats * 4;
   static constexpr int kBytes = kOffMl + 2 * NC * G * 2 * 4 + 1024;
@@ -572,9 +572,9 @@ TC_DEVICE void dec_page(const uint32_t (&qf)[DH / 16][4], uint32_t kv_smem, int 
   attn_pv<DH, 2>(s, kv_smem, 0, o);
 }
 
-template <int DH, int G, int NC>
+template <int DH, int G, int NC, int RING = kDecRingBytes>
 __global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  using SM = DecodeSmem<DH, G, NC>;
+  using SM = DecodeSmem<DH, G, NC, RING>;
   constexpr int S = SM::kStages;
   constexpr int V = DH / 32;
   extern __shared__ uint8_t attn_smem_raw[];

@@ -203,6 +203,11 @@ void init_kernel_attrs(int dev) {
   attr((const void*)tc::attn_decode<64, 2, 6>, tc::DecodeSmem<64, 2, 6>::kBytes);
   attr((const void*)tc::attn_decode<128, 4, 6>, tc::DecodeSmem<128, 4, 6>::kBytes);
   attr((const void*)tc::attn_decode<128, 5, 6>, tc::DecodeSmem<128, 5, 6>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 4, 96 * 1024>, tc::DecodeSmem<128, 4, 4, 96 * 1024>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 4, 128 * 1024>, tc::DecodeSmem<128, 4, 4, 128 * 1024>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 4, 160 * 1024>, tc::DecodeSmem<128, 4, 4, 160 * 1024>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 6, 96 * 1024>, tc::DecodeSmem<128, 4, 6, 96 * 1024>::kBytes);
+  attr((const void*)tc::attn_decode<128, 4, 6, 144 * 1024>, tc::DecodeSmem<128, 4, 6, 144 * 1024>::kBytes);
   done.insert(dev);
 }
 
@@ -655,6 +660,13 @@ struct tc_event {
   int32_t peer = 0;                 // 1 if source and destination are on different GPUs
 };
 
+// Another process's KV pool mapped into this one (CUDA IPC).
+struct tc_remote_pool {
+  int device = 0;        // device the mapping was opened on (the importer's)
+  void* base = nullptr;  // peer (or same-GPU) pointer to the exporter's pool
+  int64_t page_bytes = 0, n_pages = 0;
+};
+
 struct tc_instance {
   tc_instance_desc desc{};
   tc_model_dims d{};
@@ -709,7 +721,7 @@ struct tc_instance {
   // migration: one high-priority copy stream per destination (copies to different destinations
   // overlap each other and this instance's steps); tail = this instance's step stream position a
   // copy must follow (a step in flight may still write the request's newest row)
-  std::unordered_map<const tc_instance*, cudaStream_t> mig_streams;
+  std::unordered_map<const void*, cudaStream_t> mig_streams;  // key: destination instance / remote pool
   cudaEvent_t mig_tail = nullptr;
   tc_event* last_mig = nullptr;  // tc_kv_migrate / tc_kv_migrate_wait (synchronous form)
   int mig_ctas = 0;              // copy kernel grid (0 = 2 x SMs)
@@ -932,21 +944,35 @@ struct ProfScope {
   }
 };
 
-// decode attention consumer warps (TC_DEC_NC=4|6, A/B)
-int dec_nc() {
-  static const int nc = [] {
-    const char* e = std::getenv("TC_DEC_NC");
-    return e && std::atoi(e) == 6 ? 6 : 4;
+// decode attention variant (A/B): TC_DEC_CFG="<consumer warps>:<ring KiB>" (4:192 default; 6:192,
+// and at head_dim 128 / group 4 also 4:96, 4:128, 4:160, 6:96, 6:144); TC_DEC_GRID caps the grid
+std::pair<int, int> dec_cfg() {
+  static const std::pair<int, int> c = [] {
+    int nc = 4, kb = 192;
+    if (const char* e = std::getenv("TC_DEC_CFG")) std::sscanf(e, "%d:%d", &nc, &kb);
+    return std::make_pair(nc, kb);
   }();
-  return nc;
+  return c;
+}
+
+template <int DH, int G, int NC, int RING>
+void launch_dec_k(tc_instance* I, const tc::AttnParams& p, int dec_grid) {
+  launch_k(tc::attn_decode<DH, G, NC, RING>, dec_grid, tc::dec_threads(NC), tc::DecodeSmem<DH, G, NC, RING>::kBytes,
+           I->stream, I->kv_map, p);
 }
 
 template <int DH, int G>
 void launch_decode(tc_instance* I, const tc::AttnParams& p, int dec_grid) {
-  if (dec_nc() == 6)
-    launch_k(tc::attn_decode<DH, G, 6>, dec_grid, tc::dec_threads(6), tc::DecodeSmem<DH, G, 6>::kBytes, I->stream, I->kv_map, p);
-  else
-    launch_k(tc::attn_decode<DH, G, 4>, dec_grid, tc::dec_threads(4), tc::DecodeSmem<DH, G, 4>::kBytes, I->stream, I->kv_map, p);
+  const auto c = dec_cfg();
+  if constexpr (DH == 128 && G == 4) {
+    if (c == std::make_pair(4, 96)) return launch_dec_k<DH, G, 4, 96 * 1024>(I, p, dec_grid);
+    if (c == std::make_pair(4, 128)) return launch_dec_k<DH, G, 4, 128 * 1024>(I, p, dec_grid);
+    if (c == std::make_pair(4, 160)) return launch_dec_k<DH, G, 4, 160 * 1024>(I, p, dec_grid);
+    if (c == std::make_pair(6, 96)) return launch_dec_k<DH, G, 6, 96 * 1024>(I, p, dec_grid);
+    if (c == std::make_pair(6, 144)) return launch_dec_k<DH, G, 6, 144 * 1024>(I, p, dec_grid);
+  }
+  if (c.first == 6) return launch_dec_k<DH, G, 6, tc::kDecRingBytes>(I, p, dec_grid);
+  launch_dec_k<DH, G, 4, tc::kDecRingBytes>(I, p, dec_grid);
 }
 
 template <int DH, int G>
@@ -1055,10 +1081,10 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     // CTA-us: ~2.5 us per 128-key tile plus ~4 us fixed per CTA (Q load, TMEM, epilogue)
     const double w_pf = (2.5 * (double)pf_tiles + 4.0 * n_qblk * m.n_kv_heads) * (m.head_dim / 128.0);
     const double dec_bytes = (double)W * ps * m.head_dim * 2 * 2;
-    // decode page-stream rate per SM and its HBM cap (bytes per us); TC_DEC_RATE="per_sm,cap" (GB/s)
+    // decode page-stream rate per SM and its HBM cap (bytes per us); TC_DEC_RATE="per_sm:cap" (GB/s)
     static const std::pair<double, double> dec_rate = [] {
       double a = 40.0, b = 5200.0;
-      if (const char* e = std::getenv("TC_DEC_RATE")) std::sscanf(e, "%lf,%lf", &a, &b);
+      if (const char* e = std::getenv("TC_DEC_RATE")) std::sscanf(e, "%lf:%lf", &a, &b);
       return std::make_pair(a * 1e3, b * 1e3);
     }();
     auto t_of = [&](int P) {
@@ -1082,7 +1108,12 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     I->pf_sms = std::max(0, std::min({want, n_qblk * m.n_kv_heads, I->sms / 2}));
   }
   const int dec_sms = I->sms - I->pf_sms;
-  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_sms, (W + 7) / 8)) : 0;
+  static const int env_dec_grid = [] {
+    const char* e = std::getenv("TC_DEC_GRID");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int dec_cap = env_dec_grid > 0 ? std::min(env_dec_grid, dec_sms) : dec_sms;
+  const int dec_grid = n_dec ? (int)std::max<long long>(1, std::min<long long>(dec_cap, (W + 7) / 8)) : 0;
   // entries: one per (CTA, segment overlap); at most n_seg + dec_grid
   const int max_entries = n_seg + dec_grid;
   // layout of the metadata block
@@ -1401,6 +1432,46 @@ void enable_peer(int a, int b) {
   done.insert({a, b});
 }
 
+// Launch the page-copy kernel on src's copy stream toward dst_key (ordered after src's in-flight
+// step); returns the event (t0 recorded before the first launch, done after the last).
+tc_event* launch_page_copy(tc_instance* src, const void* dst_key, void* dst_base, const int32_t* sp, const int32_t* dp,
+                           int64_t np, bool peer, cudaEvent_t after = nullptr) {
+  std::unique_ptr<tc_event> ev(new tc_event());
+  ev->device = src->desc.device;
+  ev->pages = np;
+  ev->bytes = np * src->page_elems * 2;
+  ev->peer = peer;
+  ev->done = std::make_shared<SharedEvent>(src->desc.device, true);
+  DeviceGuard dg(src->desc.device);
+  TC_CUDA(cudaEventCreate(&ev->t0));
+  cudaStream_t& cs = src->mig_streams[dst_key];
+  if (!cs) {
+    int lo = 0, hi = 0;
+    TC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    TC_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
+  }
+  TC_CUDA(cudaEventRecord(src->mig_tail, src->stream));
+  TC_CUDA(cudaStreamWaitEvent(cs, src->mig_tail, 0));
+  if (after) TC_CUDA(cudaStreamWaitEvent(cs, after, 0));
+  TC_CUDA(cudaEventRecord(ev->t0, cs));
+  const int64_t page_vec = src->page_elems * 2 / 16;
+  const int cap = src->mig_ctas > 0 ? src->mig_ctas : 2 * src->sms;
+  for (int64_t b0 = 0; b0 < np; b0 += tc::kMigPagesPerLaunch) {
+    tc::MigPages pl;
+    pl.n = (int)std::min<int64_t>(tc::kMigPagesPerLaunch, np - b0);
+    for (int i = 0; i < pl.n; ++i) {
+      pl.src[i] = sp[b0 + i];
+      pl.dst[i] = dp[b0 + i];
+    }
+    const int blocks = (int)std::min<int64_t>(cap, std::max<int64_t>(1, pl.n * page_vec / (512 * 4)));
+    tc::kv_migrate_pages<<<blocks, 512, 0, cs>>>(reinterpret_cast<const uint4*>(src->kv), reinterpret_cast<uint4*>(dst_base),
+                                                 pl, page_vec);
+    TC_CUDA(cudaGetLastError());
+  }
+  TC_CUDA(cudaEventRecord(ev->done->e, cs));
+  return ev.release();
+}
+
 // Asynchronous KV migration (K11): every page src holds for req (at least the first n_tokens rows;
 // a step in flight on src may have written one more row, which must travel too -- a request that
 // flows away and back within that step brings it home, engine.hpp:461-493) is pushed into freshly
@@ -1422,50 +1493,28 @@ tc_event* migrate_async(tc_instance* src, tc_instance* dst, int64_t req, int64_t
   const int64_t np = (int64_t)it->second.size();
   ensure_pages(dst, req, np * ps);
   enable_peer(src->desc.device, dst->desc.device);
-  std::unique_ptr<tc_event> ev(new tc_event());
-  ev->device = src->desc.device;
-  ev->pages = np;
-  ev->bytes = np * src->page_elems * 2;
-  ev->peer = src->desc.device != dst->desc.device;
-  ev->done = std::make_shared<SharedEvent>(src->desc.device, true);
-  {
-    DeviceGuard dg(src->desc.device);
-    TC_CUDA(cudaEventCreate(&ev->t0));
-    cudaStream_t& cs = src->mig_streams[dst];
-    if (!cs) {
-      int lo = 0, hi = 0;
-      TC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      TC_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
-    }
-    // after src's in-flight step (it may write the newest row) and after any inbound copy of req
-    TC_CUDA(cudaEventRecord(src->mig_tail, src->stream));
-    TC_CUDA(cudaStreamWaitEvent(cs, src->mig_tail, 0));
-    if (EvPtr in = inbound_pending(src, req)) TC_CUDA(cudaStreamWaitEvent(cs, in->e, 0));
-    // dst pages may be quarantined pages of an earlier copy: reclaim only hands them out once
-    // their event completed, so no ordering is needed on the destination side
-    TC_CUDA(cudaEventRecord(ev->t0, cs));
-    const std::vector<int32_t>& sp = it->second;
-    const std::vector<int32_t>& dp = dst->tables[req];
-    const int64_t page_vec = src->page_elems * 2 / 16;
-    const int cap = src->mig_ctas > 0 ? src->mig_ctas : 2 * src->sms;
-    for (int64_t b0 = 0; b0 < np; b0 += tc::kMigPagesPerLaunch) {
-      tc::MigPages pl;
-      pl.n = (int)std::min<int64_t>(tc::kMigPagesPerLaunch, np - b0);
-      for (int i = 0; i < pl.n; ++i) {
-        pl.src[i] = sp[b0 + i];
-        pl.dst[i] = dp[b0 + i];
-      }
-      const int blocks = (int)std::min<int64_t>(cap, std::max<int64_t>(1, pl.n * page_vec / (512 * 4)));
-      tc::kv_migrate_pages<<<blocks, 512, 0, cs>>>(reinterpret_cast<const uint4*>(src->kv),
-                                                   reinterpret_cast<uint4*>(dst->kv), pl, page_vec);
-      TC_CUDA(cudaGetLastError());
-    }
-    TC_CUDA(cudaEventRecord(ev->done->e, cs));
-  }
+  // after any inbound copy of req (and, inside launch_page_copy, after src's in-flight step); dst
+  // pages may be quarantined pages of an earlier copy: reclaim only hands them out once their
+  // event completed, so no ordering is needed on the destination side
+  EvPtr in = inbound_pending(src, req);
+  std::unique_ptr<tc_event> ev(launch_page_copy(src, dst, dst->kv, it->second.data(), dst->tables[req].data(), np,
+                                                src->desc.device != dst->desc.device, in ? in->e : nullptr));
   dst->inbound[req] = ev->done;
   // source pages return to the pool once the copy has read them
   release_pages(src, req, ev->done);
   return ev.release();
+}
+
+tc_event* push_pages(tc_instance* src, tc_remote_pool* dst, const int32_t* sp, const int32_t* dp, int32_t np) {
+  TC_REQUIRE(src && dst && dst->base, "push: null instance or pool");
+  TC_REQUIRE(dst->device == src->desc.device, "push: pool was imported on another device than the source's");
+  TC_REQUIRE(dst->page_bytes == src->page_elems * 2, "push: pools differ in page geometry");
+  TC_REQUIRE(np >= 0 && (np == 0 || (sp && dp)), "push: null page list");
+  for (int32_t i = 0; i < np; ++i) {
+    TC_REQUIRE(sp[i] >= 0 && sp[i] < src->n_pages, "push: source page out of range");
+    TC_REQUIRE(dp[i] >= 0 && dp[i] < dst->n_pages, "push: destination page out of range");
+  }
+  return launch_page_copy(src, dst, dst->base, sp, dp, np, true);
 }
 
 void event_wait(tc_event* ev, float* copy_ms, int64_t* bytes) {
@@ -1693,6 +1742,53 @@ tc_status tc_kv_migrate_wait(tc_instance* src, float* copy_ms, int64_t* bytes) {
     src->last_mig = nullptr;
     std::unique_ptr<tc_event, void (*)(tc_event*)> hold(ev, event_destroy);
     event_wait(ev, copy_ms, bytes);
+  });
+}
+
+tc_status tc_kv_pool_export(tc_instance* inst, void* handle, int64_t* page_bytes, int64_t* n_pages) {
+  return guarded([&] {
+    TC_REQUIRE(inst && handle, "export: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == TC_IPC_HANDLE_BYTES, "IPC handle size");
+    DeviceGuard dg(inst->desc.device);
+    cudaIpcMemHandle_t h;
+    TC_CUDA(cudaIpcGetMemHandle(&h, inst->kv));
+    std::memcpy(handle, &h, sizeof(h));
+    if (page_bytes) *page_bytes = inst->page_elems * 2;
+    if (n_pages) *n_pages = inst->n_pages;
+  });
+}
+
+tc_status tc_kv_pool_import(int32_t device, const void* handle, int64_t page_bytes, int64_t n_pages, tc_remote_pool** out) {
+  return guarded([&] {
+    TC_REQUIRE(handle && out && page_bytes > 0 && n_pages > 0, "import: bad argument");
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    std::unique_ptr<tc_remote_pool> p(new tc_remote_pool());
+    p->device = device;
+    p->page_bytes = page_bytes;
+    p->n_pages = n_pages;
+    TC_CUDA(cudaIpcOpenMemHandle(&p->base, h, cudaIpcMemLazyEnablePeerAccess));
+    *out = p.release();
+  });
+}
+
+tc_status tc_remote_pool_close(tc_remote_pool* pool) {
+  return guarded([&] {
+    if (!pool) return;
+    DeviceGuard dg(pool->device);
+    cudaDeviceSynchronize();  // no copy may still target the mapping
+    const cudaError_t e = cudaIpcCloseMemHandle(pool->base);
+    delete pool;
+    TC_CUDA(e);
+  });
+}
+
+tc_status tc_kv_push_pages(tc_instance* src, tc_remote_pool* dst, const int32_t* src_pages, const int32_t* dst_pages,
+                           int32_t n_pages, tc_event** ev) {
+  return guarded([&] {
+    TC_REQUIRE(ev, "push: null event out");
+    *ev = push_pages(src, dst, src_pages, dst_pages, n_pages);
   });
 }
 

@@ -23,7 +23,9 @@ EXPORTED = [
     "tc_kv_pool_info", "tc_kv_pages", "tc_weight_ptr", "tc_read_device", "tc_weight_value", "tc_gemm",
     "tc_copy_pages", "tc_set_profiling", "tc_phase_ms", "tc_last_error", "tc_version",
     "tc_kv_migrate_async", "tc_event_query", "tc_event_wait", "tc_event_destroy", "tc_set_migration_ctas",
+    "tc_kv_pool_export", "tc_kv_pool_import", "tc_remote_pool_close", "tc_kv_push_pages",
 ]
+IPC_HANDLE_BYTES = 64  # TC_IPC_HANDLE_BYTES
 
 
 class TaichiError(RuntimeError):
@@ -98,6 +100,10 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "tc_event_wait": (I32, [P, C.POINTER(C.c_float), C.POINTER(I64)]),
         "tc_event_destroy": (I32, [P]),
         "tc_set_migration_ctas": (I32, [P, I32]),
+        "tc_kv_pool_export": (I32, [P, P, C.POINTER(I64), C.POINTER(I64)]),
+        "tc_kv_pool_import": (I32, [I32, P, I64, I64, C.POINTER(P)]),
+        "tc_remote_pool_close": (I32, [P]),
+        "tc_kv_push_pages": (I32, [P, P, C.POINTER(I32), C.POINTER(I32), I32, C.POINTER(P)]),
         "tc_kv_pool_info": (I32, [P, C.POINTER(P), C.POINTER(I64), C.POINTER(I64)]),
         "tc_kv_pages": (I32, [P, I64, C.POINTER(I32), I32, C.POINTER(I32)]),
         "tc_weight_ptr": (I32, [P, C.c_char_p, C.POINTER(P), C.POINTER(I64), C.POINTER(I64)]),
@@ -268,6 +274,25 @@ class Instance:
     def set_migration_ctas(self, ctas: int):
         _check(load_library().tc_set_migration_ctas(self._h, ctas))
 
+    # ------------------------------------------------- cross-process migration (one process per GPU)
+    def export_pool(self) -> dict:
+        """IPC description of this instance's KV pool, picklable (send it to the pushing process)."""
+        h = (C.c_uint8 * IPC_HANDLE_BYTES)()
+        pb, npg = C.c_int64(), C.c_int64()
+        _check(load_library().tc_kv_pool_export(self._h, C.cast(h, C.c_void_p), C.byref(pb), C.byref(npg)))
+        return {"handle": bytes(h), "page_bytes": pb.value, "n_pages": npg.value, "device": self.device}
+
+    def push_pages(self, remote: "RemotePool", src_pages: Sequence[int], dst_pages: Sequence[int]) -> "MigrationEvent":
+        """Copy whole KV pages of this instance into another process's pool (tc_kv_push_pages):
+        asynchronous, after this instance's in-flight step; NVLink P2P when the pool is on a peer GPU."""
+        assert len(src_pages) == len(dst_pages)
+        n = len(src_pages)
+        sp = (C.c_int32 * max(n, 1))(*[int(x) for x in src_pages])
+        dp = (C.c_int32 * max(n, 1))(*[int(x) for x in dst_pages])
+        ev = C.c_void_p()
+        _check(load_library().tc_kv_push_pages(self._h, remote._h, sp, dp, n, C.byref(ev)))
+        return MigrationEvent(ev)
+
     # ---------------------------------------------------------------- weights / profiling
     def weight(self, name: str, dtype=np.uint16) -> np.ndarray:
         ptr, r, c = C.c_void_p(), C.c_int64(), C.c_int64()
@@ -283,6 +308,29 @@ class Instance:
         v = C.c_float()
         _check(load_library().tc_phase_ms(self._h, phase.encode(), C.byref(v)))
         return float(v.value)
+
+
+class RemotePool:
+    """Another process's KV pool mapped into this process (tc_kv_pool_import), on `device` -- the
+    device of the instance that will push into it."""
+
+    def __init__(self, exported: dict, device: int):
+        h = C.create_string_buffer(bytes(exported["handle"]), IPC_HANDLE_BYTES)
+        self._h = C.c_void_p()
+        _check(load_library().tc_kv_pool_import(device, C.cast(h, C.c_void_p), exported["page_bytes"],
+                                                exported["n_pages"], C.byref(self._h)))
+        self.page_bytes, self.n_pages = exported["page_bytes"], exported["n_pages"]
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            _check(load_library().tc_remote_pool_close(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class MigrationEvent:
