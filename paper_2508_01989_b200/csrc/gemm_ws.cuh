@@ -62,7 +62,7 @@ __device__ __forceinline__ float4 ws_ld4(const float* sb, int t, int ch) {
 // starting at global weight row fbase.
 template <int EPI>
 __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const float* sb, int t, int s, int tok, int fbase,
-                                                int pos, int kv_row) {
+                                                int pos, int kv_row, const float4 (&cs_reg)[8]) {
   if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_BIAS) {
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)tok * args.ldo + fbase + s * 32;
 #pragma unroll
@@ -150,10 +150,10 @@ __device__ __forceinline__ void ws_row_epilogue(const GemmArgs& args, const floa
       }
     }
     if (is_q || is_k) {
-      const float2* cs = r.rope_cs + (size_t)pos * half + j0;  // (cos, sin) of this row
+      // (cos, sin) of this row's pairs j0.., loaded into registers before the accumulator chunk
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {
-        const float4 c = *reinterpret_cast<const float4*>(cs + i);  // (cos, sin) x 2
+        const float4 c = cs_reg[i >> 1];  // (cos, sin) x 2
         const float a0 = lo[i], b0 = hi[i], a1 = lo[i + 1], b1 = hi[i + 1];
         lo[i] = a0 * c.x - b0 * c.y;
         hi[i] = b0 * c.x + a0 * c.y;
@@ -403,6 +403,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
 #pragma unroll 1
       for (int ci = grp; ci < n_chunks; ci += 2) {
         const int c0 = ci * 32;
+        // QKV: this thread's RoPE (cos, sin) pairs for its row phase, fetched before the TMEM read
+        // and the staging barriers so the L2 round trip overlaps them (round 1: on the critical path)
+        float4 cs_reg[8];
+        if constexpr (EPI == EPI_QKV_ROPE) {
+          const int half = args.rope.head_dim >> 1;
+          const int j0 = (s * 16) % half, head = (w.nt * 256 + (int)rank * 128) / args.rope.head_dim + (s * 16) / half;
+          if (head < args.rope.n_heads + args.rope.n_kv_heads && w.mt * TN + c0 + t < args.M) {
+            const float4* cs = reinterpret_cast<const float4*>(args.rope.rope_cs + (size_t)mpos[c0 + t] * half + j0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cs_reg[i] = __ldg(cs + i);
+          }
+        }
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c0, r);
         tmem_ld_wait();
@@ -432,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
           for (int i = 0; i < 32; ++i) sb[ws_stg_idx(i, fch) + fe] = __uint_as_float(r[i]);
           asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
           const int tok = w.mt * TN + c0 + t;
-          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t]);
+          if (tok < args.M) ws_row_epilogue<EPI>(args, sb, t, s, tok, fbase, mpos[c0 + t], mkv[c0 + t], cs_reg);
         }
         if (et == 0 && grp == 0 && ci < 6) stamp(9 + ci);      // 9, 11, 13: chunk done
       }

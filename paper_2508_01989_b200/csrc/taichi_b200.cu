@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <list>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -651,6 +652,59 @@ struct KvPool {
 
 }  // namespace
 
+// Launch shape of a step: everything its kernel launches depend on besides the metadata contents.
+struct GraphKey {
+  int T, n_seq, n_qblk, n_logit, n_bt, n_seg, max_entries, dec_grid, pf_sms, meta_ints;
+  bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+
+// Instantiated step graphs by launch shape (LRU), plus the shapes seen once: a shape is captured
+// on its second occurrence, so one-off shapes never pay for instantiation.
+struct GraphCache {
+  struct Entry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int launches;
+  };
+  static constexpr size_t kCap = 24, kSeenCap = 256;
+  std::list<Entry> lru;
+  std::deque<GraphKey> seen_once;
+  const Entry* find(const GraphKey& k) {
+    for (auto it = lru.begin(); it != lru.end(); ++it)
+      if (it->key == k) {
+        lru.splice(lru.begin(), lru, it);
+        return &lru.front();
+      }
+    return nullptr;
+  }
+  bool seen(const GraphKey& k) {
+    for (const GraphKey& x : seen_once)
+      if (x == k) return true;
+    seen_once.push_back(k);
+    if (seen_once.size() > kSeenCap) seen_once.pop_front();
+    return false;
+  }
+  void put(const GraphKey& k, cudaGraphExec_t ex, int launches) {
+    lru.push_front(Entry{k, ex, launches});
+    if (lru.size() > kCap) {
+      cudaGraphExecDestroy(lru.back().exec);
+      lru.pop_back();
+    }
+  }
+  void clear() {
+    for (Entry& e : lru) cudaGraphExecDestroy(e.exec);
+    lru.clear();
+  }
+};
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TC_GRAPH");
+    return !(e && e[0] == '0') && std::getenv("TC_WS_TRACE") == nullptr;
+  }();
+  return on;
+}
+
 // An asynchronous KV migration (tc_kv_migrate_async): copy-done event + timing.
 struct tc_event {
   EvPtr done;                       // copy finished (destination pages valid, source pages reusable)
@@ -726,6 +780,7 @@ struct tc_instance {
   tc_event* last_mig = nullptr;  // tc_kv_migrate / tc_kv_migrate_wait (synchronous form)
   int mig_ctas = 0;              // copy kernel grid (0 = 2 x SMs)
   PhaseTimer prof;
+  GraphCache graphs;
 };
 
 namespace {
@@ -1243,6 +1298,23 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   I->h2d_bytes = (int64_t)off * 4;
   for (const EvPtr& e : waits) TC_CUDA(cudaStreamWaitEvent(s, e->e, 0));
   TC_CUDA(cudaEventRecord(I->ev_start, s));
+  // The step's ~230 launches go out as one CUDA graph when this launch shape has been seen before
+  // (the metadata block is re-read from pinned host memory by the graph's memcpy node, so only the
+  // shape -- grids and metadata offsets -- has to match). TC_GRAPH=0 disables it.
+  const GraphKey gkey{T, n_seq, n_qblk, n_logit, n_bt, n_seg, max_entries, dec_grid, I->pf_sms, (int)off};
+  const bool graph_ok = graphs_enabled() && !I->prof.on && waits.empty();
+  if (graph_ok) {
+    if (const GraphCache::Entry* ge = I->graphs.find(gkey)) {
+      TC_CUDA(cudaGraphLaunch(ge->exec, s));
+      I->launches = ge->launches;
+      TC_CUDA(cudaEventRecord(I->ev_stop, s));
+      I->step_pending = true;
+      I->last_sampled = n_logit;
+      return;
+    }
+  }
+  const bool capture = graph_ok && I->graphs.seen(gkey);
+  if (capture) TC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   TC_CUDA(cudaMemcpyAsync(I->meta_dev, h, off * 4, cudaMemcpyHostToDevice, s));
   const int32_t* dm = I->meta_dev;
 
@@ -1358,6 +1430,16 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     TC_CUDA(cudaMemcpyAsync(I->ids_host, I->ids_dev, (size_t)n_logit * 4, cudaMemcpyDeviceToHost, s));
   }
   TC_CUDA(cudaGetLastError());
+  if (capture) {
+    cudaGraph_t g = nullptr;
+    TC_CUDA(cudaStreamEndCapture(s, &g));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    TC_CUDA(e);
+    I->graphs.put(gkey, ex, I->launches);
+    TC_CUDA(cudaGraphLaunch(ex, s));
+  }
   TC_CUDA(cudaEventRecord(I->ev_stop, s));
   I->step_pending = true;
   I->last_sampled = n_logit;
@@ -1387,6 +1469,7 @@ void event_destroy(tc_event* ev);
 void destroy(tc_instance* I) {
   DeviceGuard dg(I->desc.device);
   if (I->stream) cudaStreamSynchronize(I->stream);
+  I->graphs.clear();
   for (auto& kv : I->mig_streams) {
     cudaStreamSynchronize(kv.second);
     cudaStreamDestroy(kv.second);
