@@ -39,10 +39,17 @@ namespace taichi {
 
 enum class ClockMode { Logical, Device };
 
+// Physical KV pool exhausted: the run's logical capacities (cluster.hpp) exceed what the GPU
+// pool can hold (taichi_serve --kv-cap keeps them consistent); reported apart from SLO misses.
+struct PoolExhausted : pdsim::EngineError {
+  using pdsim::EngineError::EngineError;
+};
+
 inline void tc_check(tc_status s, const char* what) {
   if (s == TC_OK) return;
   const std::string msg = std::string(what) + ": " + tc_last_error();
   if (s == TC_ERR_INVALID) throw pdsim::ConfigError(msg);
+  if (s == TC_ERR_OOM) throw PoolExhausted(msg);
   throw pdsim::EngineError(msg);
 }
 

@@ -3,6 +3,7 @@
 //   taichi_serve --config F [--seed S] [--model tiny|llama3_8b|qwen2_5_14b[:Ln]]
 //                [--devices 0,1,..] [--clock logical|device] [--pool-tokens N]
 //                [--log OUT] [--tokens OUT.jsonl] [--share-weights 0|1] [--link-gbps G]
+//                [--kv-cap config|auto|N]
 //
 // --clock logical: the cost model prices every step/transfer (schedule byte-identical to the
 //   reference's, checked against the oracle log) while every step really runs on the GPU and
@@ -17,6 +18,11 @@
 // and in device mode a same-device KV copy is priced at --link-gbps (default 900, the nominal
 // NVLink 5 per-direction bandwidth -- an assumption, not a measurement on this 1-GPU pool)
 // instead of its HBM-local copy time.
+// --kv-cap: the instances' logical KV capacity (cluster.kv_capacity_tokens, the scheduler's own
+//   admission control). "config" keeps the config's; "auto" caps it so the logical capacities of
+//   the instances sharing a GPU sum to 60% of that GPU's physical pool (the rest holds in-flight
+//   prefills, pending Init transfers and KV in transit, none of which the logical accounting
+//   counts); N sets it. Physical exhaustion exits with code 3 ("pool exhausted"), not an SLO miss.
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -45,6 +51,7 @@ int main(int argc, char** argv) {
   long long seed = -1, pool_tokens = 0;
   int share_weights = 1;
   double link_gbps = 900.0;
+  std::string kv_cap = "config";
   unsigned long long weight_seed = 1;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
@@ -59,6 +66,7 @@ int main(int argc, char** argv) {
     else if (k == "--weight-seed") weight_seed = std::stoull(v);
     else if (k == "--share-weights") share_weights = std::stoi(v);
     else if (k == "--link-gbps") link_gbps = std::stod(v);
+    else if (k == "--kv-cap") kv_cap = v;
     else {
       std::fprintf(stderr, "unknown flag %s\n", k.c_str());
       return 2;
@@ -111,6 +119,24 @@ int main(int argc, char** argv) {
       taichi::tc_check(tc_instance_create(&d, &h), "tc_instance_create");
       insts.push_back(h);
     }
+    if (kv_cap != "config") {
+      // logical capacity per instance from the physical pool of its GPU
+      std::vector<long long> pool_pages(insts.size(), 0), on_dev(insts.size(), 0);
+      for (std::size_t i = 0; i < insts.size(); ++i) {
+        int64_t held = 0, free_pages = 0;
+        taichi::tc_check(tc_kv_stats(insts[i], -1, &held, &free_pages), "tc_kv_stats");
+        pool_pages[i] = free_pages;
+        for (std::size_t j = 0; j < insts.size(); ++j) on_dev[i] += inst_dev[j] == inst_dev[i];
+      }
+      for (std::size_t i = 0; i < in.instances.size(); ++i) {
+        const Tokens cap = kv_cap == "auto" ? static_cast<Tokens>(0.6 * 16.0 * static_cast<double>(pool_pages[i]) /
+                                                                  static_cast<double>(on_dev[i]))
+                                            : static_cast<Tokens>(std::stoll(kv_cap));
+        in.instances[i].kv_capacity = std::min(in.instances[i].kv_capacity, cap);
+      }
+      std::fprintf(stderr, "kv-cap %s: logical capacity %lld tokens per instance\n", kv_cap.c_str(),
+                   (long long)in.instances[0].kv_capacity);
+    }
     if (clock != "logical" && clock != "device" && clock != "wall") throw ConfigError("--clock: logical|device");
     const bool device_clock = clock != "logical";
     taichi::GpuExecutor exec(insts, recs, dims.vocab, s, device_clock ? taichi::ClockMode::Device : taichi::ClockMode::Logical);
@@ -157,6 +183,9 @@ int main(int argc, char** argv) {
   } catch (const ConfigError& e) {
     std::fprintf(stderr, "config error: %s\n", e.what());
     rc = 1;
+  } catch (const taichi::PoolExhausted& e) {
+    std::fprintf(stderr, "pool exhausted: %s\n", e.what());
+    rc = 3;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     rc = 2;

@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--model", default="llama3_8b")
     ap.add_argument("--devices", default="0")
     ap.add_argument("--pool-tokens", type=int, default=0)
+    ap.add_argument("--kv-cap", default="auto",
+                    help="taichi_serve --kv-cap: logical KV capacity consistent with the physical pool (auto), "
+                         "the config's (config) or N tokens")
     ap.add_argument("--n-requests", type=int, default=0)
     ap.add_argument("--profile", default="", help="calibration JSON whose 'profile' replaces the config's")
     ap.add_argument("--slo", default="", help="TTFT_ms,TPOT_ms override of the config's SLO (config-4 SLO sets)")
@@ -71,8 +74,12 @@ def main():
                        str(sd), "--model", args.model, "--devices", args.devices, "--clock", "wall"]
                 if args.pool_tokens:
                     cmd += ["--pool-tokens", str(args.pool_tokens)]
+                cmd += ["--kv-cap", args.kv_cap]
                 t0 = time.time()
                 p = subprocess.run(cmd, capture_output=True, text=True)
+                if p.returncode == 3:  # physical KV pool exhausted: an invalid point, not an SLO miss
+                    runs.append({"seed": sd, "invalid": "pool exhausted", "error": p.stderr.strip()[-300:]})
+                    continue
                 if p.returncode != 0:
                     runs.append({"seed": sd, "error": p.stderr.strip()[-300:]})
                     atts.append(0.0)
@@ -81,10 +88,16 @@ def main():
                 s["seed"], s["host_s"] = sd, time.time() - t0
                 runs.append(s)
                 atts.append(s["attainment"])
+            if not atts:  # every seed invalid
+                pts.append({"qps": q, "mean_attainment": None, "passed": False, "invalid": True, "runs": runs})
+                print(mode, q, "INVALID (pool exhausted)", flush=True)
+                continue
             mean = sum(atts) / len(atts)
-            pts.append({"qps": q, "mean_attainment": mean, "passed": mean >= target, "runs": runs})
+            pts.append({"qps": q, "mean_attainment": mean, "passed": mean >= target, "runs": runs,
+                        "seeds_valid": len(atts), "seeds": len(seeds)})
             print(mode, q, round(mean, 4), [r.get("p90_ttft_ms") for r in runs], [r.get("p90_tpot_ms") for r in runs],
                   flush=True)
+        # goodput: the highest passing grid QPS (metrics.hpp:198-209); invalid points never pass
         good = max([p["qps"] for p in pts if p["passed"]], default=0.0)
         results["modes"][mode] = {"goodput_qps": good, "points": pts}
         print("GOODPUT", mode, good, flush=True)
