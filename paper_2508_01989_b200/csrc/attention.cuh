@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 // when a row's max grows by more than 2^8, which after the first page is rare).
 constexpr int kDecRingBytes = 192 * 1024;  // default ring (RING template parameter: A/B)
 constexpr float kDecRescaleLog2 = 8.f;  // lazy base: p = 2^(s - base) <= 2^8, P stays in bf16 range
-__host__ __device__ constexpr int dec_threads(int nc) { return (nc + 2) * 32; }
+__host__ __device__ constexpr int dec_threads(int nc, int np) { return (nc + np + 1) * 32; }
 
 template <int DH, int G, int NC, int RING = kDecRingBytes>
 struct DecodeSmem {
@@ -572,10 +572,11 @@ TC_DEVICE void dec_page(const uint32_t (&qf)[DH / 16][4], uint32_t kv_smem, int 
   attn_pv<DH, 2>(s, kv_smem, 0, o);
 }
 
-template <int DH, int G, int NC, int RING = kDecRingBytes>
-__global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+template <int DH, int G, int NC, int NP, int RING = kDecRingBytes>
+__global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   using SM = DecodeSmem<DH, G, NC, RING>;
   constexpr int S = SM::kStages;
+  static_assert(S % NP == 0, "decode ring: every stage must belong to one producer warp");
   constexpr int V = DH / 32;
   extern __shared__ uint8_t attn_smem_raw[];
   __shared__ uint64_t full[S], empty[S], qfull[2], qempty[2], pfull[2], pempty[2];
@@ -603,10 +604,15 @@ __global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_c
   float* part_o = reinterpret_cast<float*>(gbase + SM::kOffPart);
   float* part_ml = reinterpret_cast<float*>(gbase + SM::kOffMl);
 
-  if (warp == NC) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) tma_prefetch_desc(&kv_map);
-    int g = 0;  // stages issued
+  if (warp >= NC && warp < NC + NP) {
+    // ------------------------------------------------------------ producers
+    // NP warps issue the page stream together: warp NC + j issues stages g with g % NP == j. One
+    // issuing thread sustains only ~14 GB/s of random 8 KiB bulk copies (tools/stream_bench.cu:
+    // 2.1 / 4.1 / 6.9 TB/s chip-wide with 1 / 2 / 4 issuing warps per SM), so the round-1 single
+    // producer, not the ring depth, capped the stream at ~5.2 TB/s.
+    const int pj = warp - NC;
+    if (lane == 0 && pj == 0) tma_prefetch_desc(&kv_map);
+    int g = 0;  // stages of the stream so far
     for (int e0 = e_begin; e0 < e_end; e0 += 32) {
       // lane j holds entry e0 + j and its segment descriptor
       int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0);
@@ -620,7 +626,7 @@ __global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_c
         const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
         const int bt_off = __shfl_sync(0xffffffffu, sa.x, k), q_row = __shfl_sync(0xffffffffu, sa.z, k);
         const int kvh = __shfl_sync(0xffffffffu, sa.w, k);
-        if (lane == 0) {
+        if (lane == 0 && pj == 0) {
           const int b = e & 1;
           mbar_wait(&qempty[b], ((e >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&qfull[b], SM::kQBytes);
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_c
           const int n = min(32, pg1 - c);
           for (int j = 0; j < n; ++j, ++g) {
             const int rj = __shfl_sync(0xffffffffu, row, j);
-            if (lane == 0) {
+            if (lane == 0 && g % NP == pj) {
               const int st = g % S;
               mbar_wait(&empty[st], ((g / S) & 1) ^ 1);
               mbar_arrive_expect_tx(&full[st], SM::kStageBytes);
@@ -646,7 +652,7 @@ __global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_c
     return;
   }
 
-  if (warp == NC + 1) {
+  if (warp == NC + NP) {
     // ------------------------------------------------------------ merger
     for (int e0 = e_begin; e0 < e_end; e0 += 32) {
       int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0), sb = make_int4(0, 0, 0, 0);
@@ -783,6 +789,24 @@ __global__ void __launch_bounds__(dec_threads(NC), 1) attn_decode(const __grid_c
       if (lane == 0) mbar_arrive(&pfull[b]);  // release: the partial's stores precede the arrival
     }
   }
+}
+
+// Compiled decode variants: (consumer warps, producer warps) at the 192 KiB ring; the first is the
+// default (TC_DEC_CFG selects another for A/B).
+template <int DH, int G, typename F>
+void for_each_decode_variant_of(F&& f) {
+  f(attn_decode<DH, G, 4, 4>, DecodeSmem<DH, G, 4>::kBytes, 4, 4);
+  f(attn_decode<DH, G, 4, 2>, DecodeSmem<DH, G, 4>::kBytes, 4, 2);
+  f(attn_decode<DH, G, 4, 1>, DecodeSmem<DH, G, 4>::kBytes, 4, 1);
+  f(attn_decode<DH, G, 6, 4>, DecodeSmem<DH, G, 6>::kBytes, 6, 4);
+  f(attn_decode<DH, G, 6, 2>, DecodeSmem<DH, G, 6>::kBytes, 6, 2);
+}
+template <typename F>
+void for_each_decode_variant(F&& f) {
+  auto g = [&](auto kern, int smem, int, int) { f(kern, smem); };
+  for_each_decode_variant_of<64, 2>(g);
+  for_each_decode_variant_of<128, 4>(g);
+  for_each_decode_variant_of<128, 5>(g);
 }
 
 }  // namespace tc

@@ -42,13 +42,14 @@ constexpr int kWsSmemBytes = 232448;                   // max dynamic shared mem
 constexpr int kWsBarBytes = 256;
 constexpr int kWsMetaBytes = 2 * 2 * 256 * 4;          // per-unit-parity token metadata (pos, kv row)
 constexpr int kWsRingBudget = kWsSmemBytes - 1024 - 2 * kWsStagingFloats * 4 - kWsMetaBytes - kWsBarBytes;
-// warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 epilogue group 0 (even 32-token chunks),
+// warps 0 + 3 TMA, 1 MMA, 2 TMEM alloc, 4-7 epilogue group 0 (even 32-token chunks),
 // 8-11 epilogue group 1 (odd chunks): two groups hide each other's TMEM / smem / store latency
 constexpr int kWsThreads = 384;
 
 __host__ __device__ constexpr int ws_stage_bytes(int tn) { return kWsWBytes + (tn / 2) * kGemmBK * 2; }
+// ring depth for token tile tn: as deep as the budget allows, even (two producer warps alternate)
 __host__ __device__ constexpr int ws_stages(int tn) {
-  return ws_stage_bytes(tn) * kWsMaxStages <= kWsRingBudget ? kWsMaxStages : kWsRingBudget / ws_stage_bytes(tn);
+  return (ws_stage_bytes(tn) * kWsMaxStages <= kWsRingBudget ? kWsMaxStages : kWsRingBudget / ws_stage_bytes(tn)) & ~1;
 }
 
 // Features [4ch, 4ch + 4) of staged token row t (XOR swizzle: conflict-free transposed writes
@@ -272,7 +273,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
   if (!(warp == 0 && lane == 0)) pdl_wait();
   pdl_trigger();
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 3) {
+    // Two producer warps (0 and 3) issue the k-block stream together: warp 0 the even issue
+    // indices, warp 3 the odd ones (S is even, so every ring stage belongs to one of them). One
+    // issuing thread sustains only a limited TMA rate (tools/stream_bench.cu: 16 KiB boxes reach
+    // 4.2 / 6.6 TB/s chip-wide with 1 / 2 issuing warps per SM), which capped the decode-only
+    // weight stream.
+    const int pj = warp == 0 ? 0 : 1;
     if (lane == 0) {
       const int half_tn = TN / 2;
       const int wrow = (int)rank * 128;
@@ -283,19 +290,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
       Unit w0;
       if (ws_next(args, it, n_pairs, w0)) {
         pre = min(S, w0.k1 - w0.k0);
-        for (int i = 0; i < pre; ++i) {
+        for (int i = pj; i < pre; i += 2) {
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[i], 2 * stage_bytes);
           tma_load_2d_2sm(smem + i * stage_bytes, &map_w, &full_bar[i], (w0.k0 + i) * kGemmBK, w0.nt * 256 + wrow,
                           kEvictNormal);
         }
       }
       pdl_wait();
-      int stage = 0, issued = 0;
-      uint32_t phase = 0;
+      int issued = 0;
       it = ws_iter_begin(args, pair, n_pairs);
       Unit w;  // w.mt = token tile, w.nt = weight pair tile
       while (ws_next(args, it, n_pairs, w)) {
         for (int kb = w.k0; kb < w.k1; ++kb, ++issued) {
+          if ((issued & 1) != pj) continue;
+          const int stage = issued % S;
+          const uint32_t phase = (uint32_t)(issued / S) & 1u;
           uint8_t* st = smem + stage * stage_bytes;
           if (issued >= pre) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -304,10 +313,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWsThreads, 1)
           }
           tma_load_2d_2sm(st + kWsWBytes, &map_x, &full_bar[stage], kb * kGemmBK, w.mt * TN + (int)rank * half_tn,
                           kEvictLast);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
       }
     }

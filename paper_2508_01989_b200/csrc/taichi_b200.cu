@@ -198,17 +198,7 @@ void init_kernel_attrs(int dev) {
   attr((const void*)tc::attn_prefill_tc<64, 2>, tc::PfCfg<64, 2>::kBytes);
   attr((const void*)tc::attn_prefill_tc<128, 4>, tc::PfCfg<128, 4>::kBytes);
   attr((const void*)tc::attn_prefill_tc<128, 5>, tc::PfCfg<128, 5>::kBytes);
-  attr((const void*)tc::attn_decode<64, 2, 4>, tc::DecodeSmem<64, 2, 4>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 4>, tc::DecodeSmem<128, 4, 4>::kBytes);
-  attr((const void*)tc::attn_decode<128, 5, 4>, tc::DecodeSmem<128, 5, 4>::kBytes);
-  attr((const void*)tc::attn_decode<64, 2, 6>, tc::DecodeSmem<64, 2, 6>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 6>, tc::DecodeSmem<128, 4, 6>::kBytes);
-  attr((const void*)tc::attn_decode<128, 5, 6>, tc::DecodeSmem<128, 5, 6>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 4, 96 * 1024>, tc::DecodeSmem<128, 4, 4, 96 * 1024>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 4, 128 * 1024>, tc::DecodeSmem<128, 4, 4, 128 * 1024>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 4, 160 * 1024>, tc::DecodeSmem<128, 4, 4, 160 * 1024>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 6, 96 * 1024>, tc::DecodeSmem<128, 4, 6, 96 * 1024>::kBytes);
-  attr((const void*)tc::attn_decode<128, 4, 6, 144 * 1024>, tc::DecodeSmem<128, 4, 6, 144 * 1024>::kBytes);
+  tc::for_each_decode_variant([&](auto k, int bytes) { attr((const void*)k, bytes); });
   done.insert(dev);
 }
 
@@ -999,35 +989,27 @@ struct ProfScope {
   }
 };
 
-// decode attention variant (A/B): TC_DEC_CFG="<consumer warps>:<ring KiB>" (4:192 default; 6:192,
-// and at head_dim 128 / group 4 also 4:96, 4:128, 4:160, 6:96, 6:144); TC_DEC_GRID caps the grid
+// decode attention variant (A/B): TC_DEC_CFG="<consumer warps>:<producer warps>" (default 4:4;
+// tc::kDecVariants lists the compiled ones); TC_DEC_GRID caps the grid
 std::pair<int, int> dec_cfg() {
   static const std::pair<int, int> c = [] {
-    int nc = 4, kb = 192;
-    if (const char* e = std::getenv("TC_DEC_CFG")) std::sscanf(e, "%d:%d", &nc, &kb);
-    return std::make_pair(nc, kb);
+    int nc = 4, np = 4;
+    if (const char* e = std::getenv("TC_DEC_CFG")) std::sscanf(e, "%d:%d", &nc, &np);
+    return std::make_pair(nc, np);
   }();
   return c;
-}
-
-template <int DH, int G, int NC, int RING>
-void launch_dec_k(tc_instance* I, const tc::AttnParams& p, int dec_grid) {
-  launch_k(tc::attn_decode<DH, G, NC, RING>, dec_grid, tc::dec_threads(NC), tc::DecodeSmem<DH, G, NC, RING>::kBytes,
-           I->stream, I->kv_map, p);
 }
 
 template <int DH, int G>
 void launch_decode(tc_instance* I, const tc::AttnParams& p, int dec_grid) {
   const auto c = dec_cfg();
-  if constexpr (DH == 128 && G == 4) {
-    if (c == std::make_pair(4, 96)) return launch_dec_k<DH, G, 4, 96 * 1024>(I, p, dec_grid);
-    if (c == std::make_pair(4, 128)) return launch_dec_k<DH, G, 4, 128 * 1024>(I, p, dec_grid);
-    if (c == std::make_pair(4, 160)) return launch_dec_k<DH, G, 4, 160 * 1024>(I, p, dec_grid);
-    if (c == std::make_pair(6, 96)) return launch_dec_k<DH, G, 6, 96 * 1024>(I, p, dec_grid);
-    if (c == std::make_pair(6, 144)) return launch_dec_k<DH, G, 6, 144 * 1024>(I, p, dec_grid);
-  }
-  if (c.first == 6) return launch_dec_k<DH, G, 6, tc::kDecRingBytes>(I, p, dec_grid);
-  launch_dec_k<DH, G, 4, tc::kDecRingBytes>(I, p, dec_grid);
+  bool done = false;
+  tc::for_each_decode_variant_of<DH, G>([&](auto kern, int smem, int nc, int np) {
+    if (done || nc != c.first || np != c.second) return;
+    launch_k(kern, dec_grid, tc::dec_threads(nc, np), smem, I->stream, I->kv_map, p);
+    done = true;
+  });
+  TC_REQUIRE(done, "decode attention: TC_DEC_CFG names a variant that is not compiled");
 }
 
 template <int DH, int G>
