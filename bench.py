@@ -459,7 +459,7 @@ def main():
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=1)
+        cb = cpu_baseline(dims, P, prefix, D, ctx, n_logit, repeats=3)
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",

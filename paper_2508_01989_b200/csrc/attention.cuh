@@ -94,47 +94,6 @@ TC_DEVICE int kv_row(const AttnParams& p, int page, int head) {
   return (((page * p.n_layers + p.layer) * p.n_kv_heads + head) * 2) * kPage;
 }
 
-// S[16 x 8*NT] = Q K^T for keys [kbase, kbase + 8*NT) of the staged K blocks.
-template <int DH, int NT>
-TC_DEVICE void attn_qk(const uint32_t (&qf)[DH / 16][4], uint32_t k_smem, int kbase, float (&s)[NT][4]) {
-  const int lane = threadIdx.x % 32;
-  const int j = lane / 8, r = lane % 8;
-#pragma unroll
-  for (int t = 0; t < NT; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
-#pragma unroll
-  for (int ks = 0; ks < DH / 16; ++ks) {
-#pragma unroll
-    for (int t = 0; t < NT; t += 2) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(kv_addr<DH>(k_smem, kbase + t * 8 + (j / 2) * 8 + r, ks * 16 + (j % 2) * 8, 0), b0, b1, b2, b3);
-      mma_bf16_16816(s[t], qf[ks], b0, b1);
-      mma_bf16_16816(s[t + 1], qf[ks], b2, b3);
-    }
-  }
-}
-
-// O[16 x DH] += P[16 x 8*NT] V[keys kbase.., DH]
-template <int DH, int NT>
-TC_DEVICE void attn_pv(const float (&pr)[NT][4], uint32_t v_smem, int kbase, float (&o)[DH / 8][4]) {
-  const int lane = threadIdx.x % 32;
-  const int j = lane / 8, r = lane % 8;
-#pragma unroll
-  for (int kk = 0; kk < NT / 2; ++kk) {
-    uint32_t a[4];
-    a[0] = pack_bf16(pr[2 * kk][0], pr[2 * kk][1]);
-    a[1] = pack_bf16(pr[2 * kk][2], pr[2 * kk][3]);
-    a[2] = pack_bf16(pr[2 * kk + 1][0], pr[2 * kk + 1][1]);
-    a[3] = pack_bf16(pr[2 * kk + 1][2], pr[2 * kk + 1][3]);
-#pragma unroll
-    for (int n = 0; n < DH / 8; n += 2) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(kv_addr<DH>(v_smem, kbase + kk * 16 + (j % 2) * 8 + r, n * 8 + (j / 2) * 8, 1), b0, b1, b2, b3);
-      mma_bf16_16816(o[n], a, b0, b1);
-      mma_bf16_16816(o[n + 1], a, b2, b3);
-    }
-  }
-}
-
 // ============================================================== chunked prefill (tcgen05)
 // CTA = one q tile of 128 rows x one kv head: rows r = (token r / G, head r % G) of TT = 128/G
 // consecutive tokens of a prefill slice (the GQA group shares every K/V byte the CTA loads).
@@ -522,28 +481,47 @@ TC_DEVICE void store_out_row(__nv_bfloat16* out_row, const float (&acc)[G][DH / 
   }
 }
 
-// One page of one consumer warp: S = q K^T over the page's 16 keys (rows lane/4 and lane/4 + 8 of
-// the 16-row fragment; rows >= G carry zero q), lazy-base online softmax, O += P V.
+TC_DEVICE uint32_t movmatrix_trans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+
+// One page of one consumer warp, in the TRANSPOSED formulation: the page's 16 keys are the MMA's M
+// and the GQA group's heads its N (m16n8k16; G <= 8 heads, the rest zero), so a page costs
+// 8 + 8 mma.sync instead of the 16 + 16 of a 16-row q fragment with G of 16 rows live.
+//   S^T[16 keys x 8 heads] = K[16 x DH] . Q^T      (A = K via ldmatrix, B = q from registers)
+//   online softmax per head column (lanes with equal lane % 4 share a head pair), lazy base
+//   O^T[DH x 8 heads] += V^T[DH x 16 keys] . P^T   (A = V^T via ldmatrix.trans, B = P^T: the
+//                                                  S^T fragment transposed in registers by movmatrix)
+// Lane l holds keys l/4 and l/4 + 8 of heads 2(l%4) and 2(l%4) + 1: m[h], l[h], o[mt][h | 2 + h].
 template <int DH>
-TC_DEVICE void dec_page(const uint32_t (&qf)[DH / 16][4], uint32_t kv_smem, int key0, int kv_len, float scale_log2,
-                        float (&m)[2], float (&l)[2], float (&o)[DH / 8][4]) {
+TC_DEVICE void dec_page_t(const uint32_t (&qb)[DH / 16][2], uint32_t kv_smem, int key0, int kv_len, float scale_log2,
+                          float (&m)[2], float (&l)[2], float (&o)[DH / 16][4]) {
   const int lane = threadIdx.x % 32;
-  float s[2][4];
-  attn_qk<DH, 2>(qf, kv_smem, 0, s);
-  if (key0 + kPage > kv_len) {  // the segment's last page (warp-uniform)
+  const int g = lane / 4;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  {
+    // A fragment rows (keys) / column blocks of ldmatrix.x4: lane i -> key (i % 8) + 8 ((i / 8) % 2),
+    // dims 8 (i / 16) of the k-step
+    const int key = (lane % 8) + ((lane / 8) % 2) * 8, cb = (lane / 16) * 8;
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (key0 + t * 8 + (lane % 4) * 2 + (e & 1) >= kv_len) s[t][e] = -INFINITY;
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      uint32_t a[4];
+      ldsm_x4(kv_addr<DH>(kv_smem, key, ks * 16 + cb, 0), a[0], a[1], a[2], a[3]);
+      mma_bf16_16816(s, a, qb[ks][0], qb[ks][1]);
+    }
   }
-  float mx[2] = {fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1])),
-                 fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]))};
+  if (key0 + kPage > kv_len) {  // the segment's last page (warp-uniform)
+    if (key0 + g >= kv_len) s[0] = s[1] = -INFINITY;
+    if (key0 + g + 8 >= kv_len) s[2] = s[3] = -INFINITY;
+  }
+  float mx[2] = {fmaxf(s[0], s[2]), fmaxf(s[1], s[3])};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-    mx[h] *= scale_log2;  // scale > 0: the max commutes with it (-inf stays -inf)
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], off));
+    mx[h] *= scale_log2;  // scale > 0: the max commutes with it
   }
   // every page holds at least one valid key, so mx is finite; m == -inf only before the first page
   const bool grow = mx[0] > m[0] + kDecRescaleLog2 || mx[1] > m[1] + kDecRescaleLog2;
@@ -555,21 +533,27 @@ TC_DEVICE void dec_page(const uint32_t (&qf)[DH / 16][4], uint32_t kv_smem, int 
       m[h] = nb;
       l[h] *= corr;
 #pragma unroll
-      for (int n = 0; n < DH / 8; ++n) {
-        o[n][2 * h] *= corr;
-        o[n][2 * h + 1] *= corr;
+      for (int mt = 0; mt < DH / 16; ++mt) {
+        o[mt][h] *= corr;
+        o[mt][2 + h] *= corr;
       }
     }
   }
 #pragma unroll
-  for (int t = 0; t < 2; ++t)
+  for (int i = 0; i < 4; ++i) {
+    s[i] = exp2f(fmaf(s[i], scale_log2, -m[i & 1]));
+    l[i & 1] += s[i];
+  }
+  // P^T as the B operand: rows (keys 0-7 | 8-15) x heads, transposed by movmatrix
+  const uint32_t b0 = movmatrix_trans(pack_bf16(s[0], s[1])), b1 = movmatrix_trans(pack_bf16(s[2], s[3]));
+  // V^T A fragments by ldmatrix.trans: lane i -> key 8 (i / 16) + i % 8, dims 16 mt + 8 ((i / 8) % 2)
+  const int vkey = (lane / 16) * 8 + (lane % 8), vcb = ((lane / 8) % 2) * 8;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float pe = exp2f(fmaf(s[t][e], scale_log2, -m[e >> 1]));
-      s[t][e] = pe;
-      l[e >> 1] += pe;
-    }
-  attn_pv<DH, 2>(s, kv_smem, 0, o);
+  for (int mt = 0; mt < DH / 16; ++mt) {
+    uint32_t a[4];
+    ldsm_x4_t(kv_addr<DH>(kv_smem, vkey, mt * 16 + vcb, 1), a[0], a[1], a[2], a[3]);
+    mma_bf16_16816(o[mt], a, b0, b1);
+  }
 }
 
 template <int DH, int G, int NC, int NP, int RING = kDecRingBytes>
@@ -727,9 +711,7 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
   }
 
   // -------------------------------------------------------------- consumers
-  const int r_lo = lane / 4;
-  const bool ok_lo = r_lo < G;
-  const int c0 = (lane % 4) * 2;
+  const int g = lane / 4, c = lane % 4;  // key row / head pair of the transposed fragments
   int g_base = 0;  // stages before the current entry
   for (int e0 = e_begin; e0 < e_end; e0 += 32) {
     int4 ent = make_int4(0, 0, 0, 0), sa = make_int4(0, 0, 0, 0);
@@ -743,47 +725,55 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
       const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
       const int kv_len = __shfl_sync(0xffffffffu, sa.y, k);
       const int b = e & 1;
-      // q fragment (rows >= G are zero) from the entry's q slot
-      uint32_t qf[DH / 16][4];
+      // Q^T B fragments (heads >= G are zero): lane holds q[head g][16 ks + 2c .. +1] and [.. + 8 ..]
+      uint32_t qb[DH / 16][2];
       mbar_wait(&qfull[b], (e >> 1) & 1);
       {
         const __nv_bfloat16* qs = reinterpret_cast<const __nv_bfloat16*>(gbase + SM::kOffQ +
                                                                          b * ((SM::kQBytes + 127) / 128 * 128)) +
-                                  (ok_lo ? r_lo : 0) * DH + c0;
+                                  (g < G ? g : 0) * DH + c * 2;
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) {
-          qf[ks][0] = ok_lo ? *reinterpret_cast<const uint32_t*>(qs + ks * 16) : 0u;
-          qf[ks][2] = ok_lo ? *reinterpret_cast<const uint32_t*>(qs + ks * 16 + 8) : 0u;
-          qf[ks][1] = qf[ks][3] = 0u;
+          qb[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qs + ks * 16) : 0u;
+          qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qs + ks * 16 + 8) : 0u;
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[b]);
-      float o[DH / 8][4];
+      float o[DH / 16][4];
 #pragma unroll
-      for (int c = 0; c < DH / 8; ++c) o[c][0] = o[c][1] = o[c][2] = o[c][3] = 0.f;
+      for (int mt = 0; mt < DH / 16; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
       float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
       const int n = pg1 - pg0;
       // this warp's stages of the entry: g_base + i with (g_base + i) % NC == warp
       for (int i = (warp - g_base % NC + NC) % NC; i < n; i += NC) {
-        const int g = g_base + i;
-        const int st = g % S;
-        mbar_wait(&full[st], (g / S) & 1);
-        dec_page<DH>(qf, sbase + st * SM::kStageBytes, (pg0 + i) * kPage, kv_len, p.scale_log2, m, l, o);
+        const int gi = g_base + i;
+        const int st = gi % S;
+        mbar_wait(&full[st], (gi / S) & 1);
+        dec_page_t<DH>(qb, sbase + st * SM::kStageBytes, (pg0 + i) * kPage, kv_len, p.scale_log2, m, l, o);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
       }
       g_base += n;
-      l[0] += __shfl_xor_sync(0xffffffffu, l[0], 1);
-      l[0] += __shfl_xor_sync(0xffffffffu, l[0], 2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) l[h] += __shfl_xor_sync(0xffffffffu, l[h], off);
       // publish this warp's partial state (a warp without pages publishes m = -inf, l = 0, o = 0)
       mbar_wait(&pempty[b], ((e >> 1) & 1) ^ 1);  // the merger is done with entry e - 2
       float* po = part_o + ((b * NC + warp) * G) * DH;
       float* pml = part_ml + ((b * NC + warp) * G) * 2;
-      if (ok_lo) {
 #pragma unroll
-        for (int c = 0; c < DH / 8; ++c) *reinterpret_cast<float2*>(po + r_lo * DH + c * 8 + c0) = make_float2(o[c][0], o[c][1]);
-        if (lane % 4 == 0) *reinterpret_cast<float2*>(pml + r_lo * 2) = make_float2(m[0], l[0]);
+      for (int h = 0; h < 2; ++h) {
+        const int hd = 2 * c + h;
+        if (hd < G) {
+#pragma unroll
+          for (int mt = 0; mt < DH / 16; ++mt) {
+            po[hd * DH + mt * 16 + g] = o[mt][h];
+            po[hd * DH + mt * 16 + g + 8] = o[mt][2 + h];
+          }
+          if (g == 0) *reinterpret_cast<float2*>(pml + hd * 2) = make_float2(m[h], l[h]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&pfull[b]);  // release: the partial's stores precede the arrival

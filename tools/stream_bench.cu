@@ -66,7 +66,7 @@ __global__ void ldg_stream(const uint4* __restrict__ p, uint64_t n_vec, uint64_t
 // (lane 0 each) issue interleaved stages (stage k by producer k % P); `region` chunks bound the
 // random walk (TLB reach test: random over 4 GiB vs inside a few hundred MiB).
 __global__ void bulk_stream(const uint8_t* __restrict__ base, uint64_t n_chunks, int chunk, int stages, int random,
-                            int producers, uint64_t region) {
+                            int producers, uint64_t region, int lanes) {
   extern __shared__ __align__(1024) uint8_t ring[];
   __shared__ uint64_t full[64], empty[64];
   if (threadIdx.x == 0) {
@@ -80,13 +80,15 @@ __global__ void bulk_stream(const uint8_t* __restrict__ base, uint64_t n_chunks,
   const uint64_t mine = (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp < producers) {
-    if (lane == 0)
-      for (uint64_t k = warp; k < mine; k += producers) {
+    // lanes 0..lanes-1 of each producer warp issue one chunk each per round (SIMT issue)
+    if (lane < lanes)
+      for (uint64_t k = (uint64_t)warp * lanes + lane; k < mine; k += (uint64_t)producers * lanes) {
         const int st = (int)(k % stages);
         mbar_wait(&empty[st], (uint32_t)((k / stages) & 1) ^ 1);
         mbar_expect(&full[st], chunk);
         const uint64_t idx = blockIdx.x + k * gridDim.x;
-        const uint64_t c = random ? (idx / region) * region + chunk_of(idx % region, region, 1) : idx;
+        // random 1: pseudo-random over the whole buffer; 2: inside the first `region` chunks only (L2-resident)
+        const uint64_t c = random == 2 ? chunk_of(idx, region, 1) : random ? (idx / region) * region + chunk_of(idx % region, region, 1) : idx;
         const uint8_t* src = base + (c % n_chunks) * chunk;
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          smem_u32(ring + st * chunk)),
@@ -140,7 +142,46 @@ __global__ void tensor_stream(const __grid_constant__ CUtensorMap map, uint64_t 
   }
 }
 
+// 3-D boxes exactly like the decode KV stream (kv_map): {64 dims, 32 rows, 2 halves}, 128 B swizzle,
+// one 8 KiB (K, V) page-head block per box, random blocks; P producer warps
+__global__ void tensor3d_stream(const __grid_constant__ CUtensorMap map, uint64_t n_blocks, int stages, int producers) {
+  extern __shared__ __align__(1024) uint8_t ring_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ring_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[64], empty[64];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t mine = (n_blocks - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp < producers) {
+    if (lane == 0)
+      for (uint64_t k = warp; k < mine; k += producers) {
+        const int st = (int)(k % stages);
+        mbar_wait(&empty[st], (uint32_t)((k / stages) & 1) ^ 1);
+        mbar_expect(&full[st], 8192);
+        const int row = (int)(chunk_of(blockIdx.x + k * gridDim.x, n_blocks, 1) * 32);
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                smem_u32(ring + st * 8192)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(row), "r"(0), "r"(smem_u32(&full[st]))
+            : "memory");
+      }
+  } else if (warp == producers && lane == 0) {
+    for (uint64_t k = 0; k < mine; ++k) {
+      const int st = (int)(k % stages);
+      mbar_wait(&full[st], (uint32_t)((k / stages) & 1));
+      mbar_arrive(&empty[st]);
+    }
+  }
+}
+
 int main() {
+  setvbuf(stdout, nullptr, _IOLBF, 0);
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const size_t bytes = (size_t)4 << 30;  // 4 GiB: far beyond L2
@@ -156,7 +197,7 @@ int main() {
     launch();
     CK(cudaDeviceSynchronize());
     float best = 1e30f;
-    for (int r = 0; r < 5; ++r) {
+    for (int r = 0; r < 3; ++r) {
       CK(cudaEventRecord(a));
       launch();
       CK(cudaEventRecord(b));
@@ -177,24 +218,44 @@ int main() {
                   grid, thr, per_sm * thr * 8 * 16 / 1024, bytes / ms / 1e6);
     }
   }
-  for (int random : {1, 0})
-    for (int chunk : {8192, 16384})
-      for (int producers : {1, 2, 4})
-        for (uint64_t region_mb : {4096ull, 128ull, 16ull}) {
-          if (!random && region_mb != 4096) continue;
-          const int ring = 192 * 1024;
-          const int stages = ring / chunk;
-          const int grid = sms;
-          CK(cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, ring));
-          const uint64_t n = bytes / chunk - ((bytes / chunk) % 2 == 0 ? 1 : 0);
-          const uint64_t region = region_mb * (1ull << 20) / chunk - 1;
-          const float ms = time_it([&] {
-            bulk_stream<<<grid, 32 * (producers + 1), ring>>>(buf, n, chunk, stages, random, producers, region);
-          });
-          std::printf("{\"kernel\": \"bulk\", \"random\": %d, \"region_mb\": %llu, \"chunk\": %d, \"producers\": %d, "
-                      "\"ring_kb\": 192, \"gb_s\": %.1f}\n",
-                      random, (unsigned long long)region_mb, chunk, producers, (double)n * chunk / ms / 1e6);
-        }
+  {
+    PFN_cuTensorMapEncodeTiled_v12000 enc3 = nullptr;
+    cudaDriverEntryPointQueryResult q3;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc3), cudaEnableDefault, &q3));
+    const uint64_t rows = bytes / 256;  // rows of 128 dims (256 B), viewed {64 dims, rows, 2 halves}
+    CUtensorMap map;
+    cuuint64_t dims[3] = {64, rows, 2};
+    cuuint64_t strides[2] = {256, 128};
+    cuuint32_t box[3] = {64, 32, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc3(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 1;
+    const uint64_t n_blocks = rows / 32 - 1;
+    for (int producers : {1, 2, 4, 8}) {
+      const int stages = 24;
+      CK(cudaFuncSetAttribute(tensor3d_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024 + 1024));
+      const float ms = time_it([&] { tensor3d_stream<<<sms, 32 * (producers + 1), 192 * 1024 + 1024>>>(map, n_blocks, stages, producers); });
+      std::printf("{\"kernel\": \"tensor3d_kv\", \"random\": 1, \"box_bytes\": 8192, \"producers\": %d, \"gb_s\": %.1f}\n",
+                  producers, (double)n_blocks * 8192 / ms / 1e6);
+    }
+  }
+  for (int random : {1, 2})
+  for (int chunk : {2048, 8192, 16384})
+    for (int producers : {1, 2, 4})
+      for (int lanes : {1, 4, 8}) {
+        const int ring = 192 * 1024;
+        const int stages = ring / chunk;
+        if (stages % (producers * lanes)) continue;
+        CK(cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, ring));
+        const uint64_t n = (bytes / 4) / chunk - 1;  // 1 GiB per timing
+        const uint64_t region = ((random == 2 ? 32ull : 4096ull) << 20) / chunk - 1;
+        const float ms = time_it([&] {
+          bulk_stream<<<sms, 32 * (producers + 1), ring>>>(buf, n, chunk, stages, random, producers, region, lanes);
+        });
+        std::printf("{\"kernel\": \"bulk\", \"random\": %d, \"chunk\": %d, \"producers\": %d, \"lanes\": %d, "
+                    "\"gb_s\": %.1f}\n", random, chunk, producers, lanes, (double)n * chunk / ms / 1e6);
+      }
   // tensor map over the buffer as [rows, 8192 cols] bf16 (16 KiB rows), boxes 64 cols x R rows
   PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   cudaDriverEntryPointQueryResult q;
