@@ -10,8 +10,8 @@
 // (address = half*4096 + row*128 + ((chunk ^ row) & 7) * 16). Completion is tracked with
 // mbarrier transaction counts, so no thread computes per-chunk gather addresses.
 //
-//  * attn_prefill_tc -- chunked-prefill queries attend causally to the paged prefix + in-chunk
-//    keys on tcgen05 (S and O in TMEM), see its section below.
+//  * attn_prefill_tc2 -- chunked-prefill queries attend causally to the paged prefix + in-chunk
+//    keys on tcgen05 (S and O in TMEM), two q tiles per CTA, see its section below.
 //  * attn_decode   -- balanced page stream: every SM gets the same number of page-heads
 //    (contiguous range over all (request, kv head) segments); a producer warp streams
 //    K/V pages through a 24-stage TMA ring, 4 consumer warps split the pages and merge
@@ -42,7 +42,14 @@ struct AttnParams {
   float* ws_o;               // [slot][G][DH] partial o of segments cut by CTA boundaries
   float* ws_ml;              // [slot][G][2]
   int* dec_cnt;              // [seg] arrival counters (zero; the last arriver resets)
+  unsigned long long* pf_trace;  // tools only (TC_PF_TRACE): %globaltimer stamps of one attn_prefill_tc2 CTA
 };
+
+TC_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 TC_DEVICE void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -95,104 +102,127 @@ TC_DEVICE int kv_row(const AttnParams& p, int page, int head) {
 }
 
 // ============================================================== chunked prefill (tcgen05)
-// CTA = one q tile of 128 rows x one kv head: rows r = (token r / G, head r % G) of TT = 128/G
-// consecutive tokens of a prefill slice (the GQA group shares every K/V byte the CTA loads).
-// Per 128-key tile j (8 pages):
-//   MMA warp   S_j = Q K_j^T            (M=128, N=128, K=DH; Q, K in smem, SW128 K-major) -> TMEM S[j&1]
-//   softmax    8 warps, 2 threads per row (TMEM lane): warp w < 4 takes keys 0-63 of rows
-//              32w.., warp w + 4 keys 64-127; the pair exchanges its row max through smem, then
-//              writes bf16 P_j over its own S_j columns in TMEM (two keys per 32-bit column)
-//   MMA warp   O += P_j V_j             (A = P from TMEM, B = V MN-major SW128), O in TMEM
-//   softmax    lazy rescale: O and l move to a new base only when the row max grows by > 2^8
-//              (rare after the first tiles), so the loop never reads O
-// The MMA warp issues S_{j+1} before waiting for P_j, so QK^T of the next tile overlaps the
-// softmax of the current one. K and V tiles stream through separate TMA rings (3 / 2 stages, one
-// 2 KiB box per page and 64-dim half), K_j is released when S_j completes, V_j when O_j does.
-constexpr int kPfKeys = 128;
-constexpr int kPfThreads = 352;  // warps 0-7 softmax/epilogue (2 threads per row), 8 K producer, 9 V producer,
+// attn_prefill_tc2: one CTA = TWO consecutive 128-row q tiles of one slice and kv head (2 * TT
+// tokens; a q row = (token r / G, head r % G), so the GQA group shares every K/V byte), FA4-style
+// ping-pong. Both tiles share the K/V tiles the CTA stages (half the L2->SMEM traffic per query of
+// round 1's one-tile kernel), and while one softmax group works on its S tile the tensor core
+// computes the other tile's PV and next S:
+//   MMA warp   per key tile j:  PV0_{j-1}, S0_j, PV1_{j-1}, S1_j   (tcgen05 executes in issue order,
+//              so S_t,j overwrites P_t,j-1 in TMEM only after PV_t,j-1 has read it, and "S_t,j
+//              complete" implies "PV_t,j-1 complete": the lazy O rescale needs no extra wait)
+//   softmax    group t = warps 4t..4t+3, ONE thread per row: pass 1 row max over the 128 scores,
+//              lazy base (O / l move only when the max grows by > 2^8), pass 2 re-reads S from TMEM
+//              32 keys at a time (few live registers: 106 per thread, no spills) and writes P as
+//              bf16 pairs over S columns 0-63. The mask decision is warp-uniform (round 1 let the
+//              3 idle rows of a G = 5 tile drag their warp through the masked path on every tile:
+//              that warp ran ~2x longer and the MMA waited for it).
+// TMEM: S0 @0, S1 @128, O0 @256, O1 @256 + DH. The rows of tile 1 beyond the slice are skipped when
+// the slice ends inside tile 0 (`two` false).
+// Measured (Qwen2.5-14B config 5, %globaltimer trace TC_PF_TRACE=1): ~2.3 us per 128-key tile for
+// both q tiles (tensor pipe busy ~1.5 us of it); round 1's one-tile kernel: ~4 us per q tile.
+// Tried and dropped: FA4's polynomial exp2 on the FMA pipe for 1/2 or 3/4 of the scores (slower:
+// the polynomial costs ~10 issue slots against MUFU.EX2's 8-cycle pipe occupancy, tools/xu_bench.cu),
+// and issuing PV per 32-key chunk as the softmax publishes it (slower: a tcgen05.wait::st per chunk).
+constexpr int kPfKeys = 128;     // keys per S tile
+constexpr int kPfThreads = 352;  // warps 0-7 softmax / epilogue, 8 Q + K producer, 9 V producer,
                                  // 10 MMA issuer + TMEM owner
-constexpr int kPfStages = 3;   // K ring depth
-constexpr int kPfVStages = 2;  // V ring depth (V_j is consumed one MMA later than K_j)
+constexpr int kPf2KStages = 2;
+constexpr int kPf2VStages = 2;
 
 template <int DH, int G>
-struct PfCfg {
-  static constexpr int TT = 128 / G;                 // tokens per q tile
+struct Pf2Cfg {
+  static constexpr int TT = 128 / G;
   static constexpr int kHalves = DH / 64;
-  static constexpr int kSlab = 128 * 128;            // 128 rows x 128 B
-  static constexpr int kQBytes = kHalves * kSlab;    // Q [128 rows][DH]
-  static constexpr int kKBytes = kHalves * kSlab;    // K [128 keys][DH] (one slab per 64-dim half)
+  static constexpr int kSlab = 128 * 128;          // 128 rows x 128 B
+  static constexpr int kQBytes = kHalves * kSlab;  // one q tile [128 rows][DH]
+  static constexpr int kKBytes = kHalves * kSlab;  // one K or V tile [128 keys][DH]
   static constexpr int kOffQ = 0;
-  static constexpr int kOffK = kQBytes;
-  static constexpr int kOffV = kOffK + kPfStages * kKBytes;
-  static constexpr int kOffX = kOffV + kPfVStages * kKBytes;  // row-max / row-sum exchange [2][2][128] f32
-  static constexpr int kBytes = kOffX + 2 * 2 * 128 * 4 + 1024;
-  static constexpr uint32_t kQTx = kHalves * TT * G * 128;  // bytes the Q boxes deliver
+  static constexpr int kOffK = 2 * kQBytes;
+  static constexpr int kOffV = kOffK + kPf2KStages * kKBytes;
+  static constexpr int kBytes = kOffV + kPf2VStages * kKBytes + 1024;
+  static constexpr uint32_t kQTx = kHalves * TT * G * 128;  // bytes the Q boxes of one tile deliver
   static_assert(kBytes <= 227 * 1024, "prefill smem");
 };
 
 template <int DH, int G>
 __global__ void __launch_bounds__(kPfThreads, 1)
-    attn_prefill_tc(const __grid_constant__ CUtensorMap kv2_map, const __grid_constant__ CUtensorMap q_map, AttnParams p) {
-  using C = PfCfg<DH, G>;
+    attn_prefill_tc2(const __grid_constant__ CUtensorMap kv2_map, const __grid_constant__ CUtensorMap q_map, AttnParams p) {
+  using C = Pf2Cfg<DH, G>;
   constexpr int TT = C::TT;
+  constexpr int KS = kPf2KStages, VS = kPf2VStages;
   extern __shared__ uint8_t attn_smem_raw[];
-  __shared__ uint64_t q_full, k_full[kPfStages], k_empty[kPfStages], v_full[kPfVStages], v_empty[kPfVStages];
+  __shared__ uint64_t q_full, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS];
   __shared__ uint64_t s_full[2], p_full[2], o_full[2];
   __shared__ uint32_t tmem_slot;
   const uint32_t sbase = (smem_u32(attn_smem_raw) + 1023u) & ~1023u;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // grid (kv heads, q blocks): all heads of the longest q block are dispatched first (the host
-  // sorts the q-block list longest-first)
   const int seq = p.qblk_seq[blockIdx.y];
   const int qoff = p.qblk_off[blockIdx.y];
   const int kvh = blockIdx.x;
   const int q_start = p.seq_q_start[seq], q_len = p.seq_q_len[seq], pos0 = p.seq_pos0[seq];
   const int* bt = p.block_tables + p.seq_bt_off[seq];
-  const int kv_end = pos0 + min(qoff + TT, q_len);
+  const bool two = qoff + TT < q_len;
+  const int nq = two ? 2 : 1;
+  const int kv_end = pos0 + min(qoff + nq * TT, q_len);
   const int n_tiles = (kv_end + kPfKeys - 1) / kPfKeys;
   const int n_pages = (kv_end + kPage - 1) / kPage;
+  // tools only: CTA (0, 1) (a full two-tile work item; the longest-first order puts a tail first)
+  unsigned long long* trc = (p.pf_trace && blockIdx.x == 0 && blockIdx.y == min(1, (int)gridDim.y - 1)) ? p.pf_trace : nullptr;
+  auto stamp = [&](int j, int k) {  // trace slot [key tile j < 64][k < 16]
+    if (trc && j < 64) trc[j * 16 + k] = gtimer();
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
-    for (int s = 0; s < kPfStages; ++s) {
+    for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
     }
-    for (int s = 0; s < kPfVStages; ++s) {
+    for (int s = 0; s < VS; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 256);
-      mbar_init(&o_full[b], 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_full[t], 1);
     }
     mbar_fence_init();
   }
   if (warp == 10) tmem_alloc(&tmem_slot, 512);
+  if constexpr (TT * G < 128) {
+    // q rows TT*G..127 of both tiles are never loaded: zero them so their S rows stay finite and
+    // every row of a warp can take the unmasked softmax path (no per-lane divergence)
+    for (int i = threadIdx.x; i < 2 * C::kHalves * (128 - TT * G) * 8; i += blockDim.x) {
+      const int chunk = i % 8, row = TT * G + (i / 8) % (128 - TT * G), slab = i / (8 * (128 - TT * G));
+      *reinterpret_cast<uint4*>(attn_smem_raw + (sbase - smem_u32(attn_smem_raw)) + C::kOffQ + slab * C::kSlab + row * 128 +
+                                chunk * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;  // S0 @0, S1 @128, O0 @256, O1 @384
-  pdl_wait();  // q / K / V written by the QKV GEMM (the step metadata above came from a memcpy)
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();  // q / K / V written by the QKV GEMM
   pdl_trigger();
 
   if (warp == 8 || warp == 9) {
-    // ------------------------------------------------------------ TMA producers: warp 8 streams
-    // Q then the K tiles, warp 9 the V tiles, so a K load never waits for a V slot (V_j frees one
-    // MMA later than K_j)
+    // ------------------------------------------------------------ TMA producers: warp 8 Q + K, warp 9 V
     const bool is_v = warp == 9;
     if (lane == 0 && !is_v) {
       tma_prefetch_desc(&kv2_map);
       tma_prefetch_desc(&q_map);
-      mbar_arrive_expect_tx(&q_full, C::kQTx);
+      mbar_arrive_expect_tx(&q_full, nq * C::kQTx);
+      for (int t = 0; t < nq; ++t)
 #pragma unroll
-      for (int h = 0; h < C::kHalves; ++h)
-        tma_load_3d(sbase + C::kOffQ + h * C::kSlab, &q_map, &q_full, h * 64, kvh * G, q_start + qoff);
+        for (int h = 0; h < C::kHalves; ++h)
+          tma_load_3d(sbase + C::kOffQ + t * C::kQBytes + h * C::kSlab, &q_map, &q_full, h * 64, kvh * G,
+                      q_start + qoff + t * TT);
     }
     auto page_id = [&](int gp) { return bt[gp < n_pages ? gp : 0]; };  // beyond the sequence: masked
     int cur = lane < 8 ? page_id(lane) : 0;
-    const int depth = is_v ? kPfVStages : kPfStages;
+    const int depth = is_v ? VS : KS;
     uint64_t* fullb = is_v ? v_full : k_full;
     uint64_t* emptyb = is_v ? v_empty : k_empty;
     const uint32_t ring = sbase + (is_v ? C::kOffV : C::kOffK);
@@ -219,158 +249,171 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, kPfKeys);
     constexpr uint32_t idesc_o = umma_idesc_bf16_bmn(128, DH);
-    auto issue_pv = [&](int i) {
-      const int st = i % kPfVStages;
-      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
-      mbar_wait(&v_full[st], (i / kPfVStages) & 1);
+    auto issue_s = [&](int t, int j) {
+      const int st = j % KS;
+      if (elect_one()) {
+        const uint32_t kb = sbase + C::kOffK + st * C::kKBytes;
+        const uint32_t qb = sbase + C::kOffQ + t * C::kQBytes;
+#pragma unroll
+        for (int h = 0; h < C::kHalves; ++h)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + t * 128, umma_smem_desc<128>(qb + h * C::kSlab + k * 32),
+                      umma_smem_desc<128>(kb + h * C::kSlab + k * 32), idesc_s, (h | k) ? 1u : 0u);
+        umma_commit(&s_full[t]);
+        if (t == nq - 1) umma_commit(&k_empty[st]);
+      }
+      __syncwarp();
+    };
+    // (measured: issuing PV per 32-key chunk as the softmax publishes it was slower -- the extra
+    // tcgen05.wait::st per chunk lengthens the softmax more than the early PV start saves)
+    auto issue_pv = [&](int t, int i) {
+      const int st = i % VS;
+      mbar_wait(&p_full[t], i & 1);
+      if (t == 0) mbar_wait(&v_full[st], (i / VS) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t vb = sbase + C::kOffV + st * C::kKBytes;
-        // P of keys 0-63 sits at S columns 0-31, keys 64-127 at S columns 64-95 (each softmax
-        // thread overwrites only the S columns it has read itself)
 #pragma unroll
         for (int kk = 0; kk < kPfKeys / 16; ++kk)
-          umma_bf16_tmem_a(tmem + 256, tmem + (i & 1) * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
-                           umma_smem_desc_mn128(vb + kk * 2048, C::kSlab, 1024), idesc_o, (i | kk) ? 1u : 0u);
-        umma_commit(&o_full[i & 1]);
-        umma_commit(&v_empty[st]);
+          umma_bf16_tmem_a(tmem + 256 + t * DH, tmem + t * 128 + kk * 8, umma_smem_desc_mn128(vb + kk * 2048, C::kSlab, 1024),
+                           idesc_o, (i | kk) ? 1u : 0u);
+        umma_commit(&o_full[t]);
+        if (t == nq - 1) umma_commit(&v_empty[st]);
       }
       __syncwarp();
     };
     mbar_wait(&q_full, 0);
     for (int j = 0; j < n_tiles; ++j) {
-      const int st = j % kPfStages;
-      mbar_wait(&k_full[st], (j / kPfStages) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t kb = sbase + C::kOffK + st * C::kKBytes;
-#pragma unroll
-        for (int h = 0; h < C::kHalves; ++h)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + (j & 1) * 128, umma_smem_desc<128>(sbase + C::kOffQ + h * C::kSlab + k * 32),
-                      umma_smem_desc<128>(kb + h * C::kSlab + k * 32), idesc_s, (h | k) ? 1u : 0u);
-        umma_commit(&s_full[j & 1]);
-        umma_commit(&k_empty[st]);
+      for (int t = 0; t < nq; ++t) {
+        if (j >= 1) issue_pv(t, j - 1);
+
+        if (t == 0) {
+          mbar_wait(&k_full[j % KS], (j / KS) & 1);
+          tc_fence_after();
+
+        }
+        issue_s(t, j);
       }
-      __syncwarp();
-      if (j >= 1) issue_pv(j - 1);
     }
-    issue_pv(n_tiles - 1);
-  } else {
-    // ------------------------------------------------------------ softmax / epilogue
-    constexpr int HD = DH / 2;             // head dims per thread
-    const int quarter = warp & 3, half = warp >> 2;
-    const int r = quarter * 32 + lane;     // row == TMEM lane
-    const int t = r / G, g = r % G;
-    const bool valid = r < TT * G && qoff + t < q_len;
-    const int lim = valid ? pos0 + qoff + t + 1 : 0;  // causal: keys < lim
+    for (int t = 0; t < nq; ++t) issue_pv(t, n_tiles - 1);
+  } else if ((warp >> 2) < nq) {
+    // ------------------------------------------------------------ softmax / epilogue of q tile t
+    const int t = warp >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // row == TMEM lane
+    const int tok = qoff + t * TT + r / G, g = r % G;
+    const bool valid = r < TT * G && tok < q_len;
+    // causal: keys < lim. Rows outside the slice are never stored; they take every key (finite
+    // scores of zero / foreign q rows) so a warp's mask decision stays uniform.
+    const int lim = valid ? pos0 + tok + 1 : 0x7fffffff;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    float* xmax = reinterpret_cast<float*>(attn_smem_raw + (sbase - smem_u32(attn_smem_raw)) + C::kOffX);  // [2][2][128]
-    // O accumulates in TMEM across tiles relative to a per-row base m_used; the base moves (and
-    // O, l are rescaled) only when the row max exceeds it by more than 2^8, so P <= 256 in bf16.
+    const uint32_t s_addr = tmem + lane_off + t * 128;
+    const uint32_t o_addr = tmem + lane_off + 256 + t * DH;
     constexpr float kRescale = 8.f;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const uint32_t s_addr = tmem + lane_off + (j & 1) * 128 + half * 64;
-      const int key0 = j * kPfKeys + half * 64;
-      const bool full = key0 + 63 < lim;  // no causal / length mask inside this thread's 64 keys
-      // this thread's 64 scores stay in registers for both passes (one TMEM round trip)
-      uint32_t v[64];
-      tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-      tmem_ld_32x32b_x32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-      tmem_ld_wait();
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      if (full) {
+      if (lane == 0) stamp(j, 8 + warp);  // S_t,j seen by this warp
+      const int key0 = j * kPfKeys;
+      const bool full = __all_sync(0xffffffffu, key0 + kPfKeys - 1 < lim);  // warp-uniform
+      // pass 1: row max over the 128 scores (two 64-column loads, 8 independent max chains)
+      float mx8[8];
 #pragma unroll
-        for (int x = 0; x < 64; ++x) mx4[x & 3] = fmaxf(mx4[x & 3], __uint_as_float(v[x]));
-      } else {
+      for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
 #pragma unroll
-        for (int x = 0; x < 64; ++x)
-          if (key0 + x < lim) mx4[x & 3] = fmaxf(mx4[x & 3], __uint_as_float(v[x]));
-      }
-      // pair exchange of the row max (buffer j & 1; the partner reads it before the next barrier)
-      const float mine = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
-      xmax[((j & 1) * 2 + half) * 128 + r] = mine;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-      const float mx = fmaxf(mine, xmax[((j & 1) * 2 + (half ^ 1)) * 128 + r]);  // tile row max
-      // rescale decision per row; the TMEM traffic is warp-collective (tcgen05.ld/st .sync.aligned),
-      // so a warp rescales when any of its rows needs it (factor 1 for the others)
-      const bool need = mx > m_used + kRescale;  // (also the first valid tile: m_used = -inf)
-      if (j > 0 && __any_sync(0xffffffffu, need && m_used != -INFINITY)) {
-        // O holds PV_0..PV_{j-1}: S_j complete => PV_{j-2} complete (in-order), so PV_{j-1}'s
-        // barrier phase cannot alias
-        const float corr = (need && m_used != -INFINITY) ? fast_exp2(m_used - mx) : 1.f;
-        mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-        uint32_t ov[HD];
-        const uint32_t o_addr = tmem + lane_off + 256 + half * HD;
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c)
-          tmem_ld_32x32b_x32(o_addr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t v[64];
+        tmem_ld_32x32b_x32(s_addr + hh * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        tmem_ld_32x32b_x32(s_addr + hh * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         tmem_ld_wait();
+        if (full) {
 #pragma unroll
-        for (int x = 0; x < HD; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * corr);
+          for (int x = 0; x < 64; ++x) mx8[x & 7] = fmaxf(mx8[x & 7], __uint_as_float(v[x]));
+        } else {
 #pragma unroll
-        for (int c = 0; c < HD / 16; ++c)
-          tmem_st_32x32b_x16(o_addr + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(&ov[c * 16]));
+          for (int x = 0; x < 64; ++x)
+            if (key0 + hh * 64 + x < lim) mx8[x & 7] = fmaxf(mx8[x & 7], __uint_as_float(v[x]));
+        }
+      }
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * p.scale_log2;
+      const bool need = mx > m_used + kRescale;  // (also the first tile with a valid key: m_used = -inf)
+      if (j > 0 && __any_sync(0xffffffffu, need && m_used != -INFINITY)) {
+        // O holds PV_0..PV_{j-1}, complete: S_j completed after them (in-order tensor pipe)
+        const float corr = (need && m_used != -INFINITY) ? fast_exp2(m_used - mx) : 1.f;
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld_32x32b_x32(o_addr + c * 32, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * corr);
+          tmem_st_32x32b_x16(o_addr + c * 32, *reinterpret_cast<const uint32_t(*)[16]>(&ov[0]));
+          tmem_st_32x32b_x16(o_addr + c * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(&ov[16]));
+        }
         l *= corr;
       }
       if (need) m_used = mx;
       const float base = m_used == -INFINITY ? 0.f : m_used;
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[32];
-      if (full) {
+      // pass 2, 32 keys at a time (TMEM reloads are cheap; few live registers leave the scheduler
+      // room to overlap the MUFU latency): P as bf16 pairs over S columns 16c .. 16c + 15, i.e.
+      // over scores this thread has already consumed
 #pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base));
-          sum4[x & 3] += p0 + p1;
-          pk[x] = pack_bf16(p0, p1);
-        }
-      } else {
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(s_addr + c * 32, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+        if (full) {
 #pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          const float p0 = key0 + 2 * x < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base)) : 0.f;
-          const float p1 =
-              key0 + 2 * x + 1 < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base)) : 0.f;
-          sum4[x & 3] += p0 + p1;
-          pk[x] = pack_bf16(p0, p1);
+          for (int x = 0; x < 16; ++x) {
+            const float a0 = fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base);
+            const float a1 = fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base);
+            const float p0 = fast_exp2(a0), p1 = fast_exp2(a1);
+            sum4[x & 3] += p0 + p1;
+            pk[x] = pack_bf16(p0, p1);
+          }
+        } else {
+          const int k0 = key0 + c * 32;
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            const float p0 = k0 + 2 * x < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * x]), p.scale_log2, -base)) : 0.f;
+            const float p1 =
+                k0 + 2 * x + 1 < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * x + 1]), p.scale_log2, -base)) : 0.f;
+            sum4[x & 3] += p0 + p1;
+            pk[x] = pack_bf16(p0, p1);
+          }
         }
+        tmem_st_32x32b_x16(s_addr + c * 16, pk);
       }
-      // P over this thread's already-read S columns
-      tmem_st_32x32b_x16(s_addr, *reinterpret_cast<const uint32_t(*)[16]>(&pk[0]));
-      tmem_st_32x32b_x16(s_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(&pk[16]));
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[j & 1]);
+      mbar_arrive(&p_full[t]);
+      if (lane == 0) stamp(j, warp);  // P_t,j written by this warp
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
     }
-    // O final once the last PV completes (S_{n-1} complete => PV_{n-3} complete)
-    mbar_wait(&o_full[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    // O final once the last PV completes (S_{n-1} complete => PV_{n-2} complete)
+    mbar_wait(&o_full[t], (n_tiles - 1) & 1);
     tc_fence_after();
-    uint32_t o[HD];
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = p.out + (long long)(q_start + tok) * p.n_heads * DH + (kvh * G + g) * DH;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c)
-      tmem_ld_32x32b_x32(tmem + lane_off + 256 + half * HD + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-    tmem_ld_wait();
-    // row sum = both halves' partial sums (same base)
-    xmax[half * 128 + r] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-    const float l_row = l + xmax[(half ^ 1) * 128 + r];
-    if (valid) {
-      const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
-      __nv_bfloat16* dst = p.out + (long long)(q_start + qoff + t) * p.n_heads * DH + (kvh * G + g) * DH + half * HD;
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(o_addr + c * 32, o);
+      tmem_ld_wait();
+      if (valid) {
 #pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(o[c * 8 + 0]) * inv, __uint_as_float(o[c * 8 + 1]) * inv);
-        w.y = pack_bf16(__uint_as_float(o[c * 8 + 2]) * inv, __uint_as_float(o[c * 8 + 3]) * inv);
-        w.z = pack_bf16(__uint_as_float(o[c * 8 + 4]) * inv, __uint_as_float(o[c * 8 + 5]) * inv);
-        w.w = pack_bf16(__uint_as_float(o[c * 8 + 6]) * inv, __uint_as_float(o[c * 8 + 7]) * inv);
-        st_global_v4(dst + c * 8, w);
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[q * 8 + 0]) * inv, __uint_as_float(o[q * 8 + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(o[q * 8 + 2]) * inv, __uint_as_float(o[q * 8 + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(o[q * 8 + 4]) * inv, __uint_as_float(o[q * 8 + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(o[q * 8 + 6]) * inv, __uint_as_float(o[q * 8 + 7]) * inv);
+          st_global_v4(dst + c * 32 + q * 8, w);
+        }
       }
     }
   }

@@ -195,9 +195,9 @@ void init_kernel_attrs(int dev) {
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   };
-  attr((const void*)tc::attn_prefill_tc<64, 2>, tc::PfCfg<64, 2>::kBytes);
-  attr((const void*)tc::attn_prefill_tc<128, 4>, tc::PfCfg<128, 4>::kBytes);
-  attr((const void*)tc::attn_prefill_tc<128, 5>, tc::PfCfg<128, 5>::kBytes);
+  attr((const void*)tc::attn_prefill_tc2<64, 2>, tc::Pf2Cfg<64, 2>::kBytes);
+  attr((const void*)tc::attn_prefill_tc2<128, 4>, tc::Pf2Cfg<128, 4>::kBytes);
+  attr((const void*)tc::attn_prefill_tc2<128, 5>, tc::Pf2Cfg<128, 5>::kBytes);
   tc::for_each_decode_variant([&](auto k, int bytes) { attr((const void*)k, bytes); });
   done.insert(dev);
 }
@@ -690,7 +690,7 @@ struct GraphCache {
 bool graphs_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("TC_GRAPH");
-    return !(e && e[0] == '0') && std::getenv("TC_WS_TRACE") == nullptr;
+    return !(e && e[0] == '0') && std::getenv("TC_WS_TRACE") == nullptr && std::getenv("TC_PF_TRACE") == nullptr;
   }();
   return on;
 }
@@ -1013,16 +1013,40 @@ void launch_decode(tc_instance* I, const tc::AttnParams& p, int dec_grid) {
 }
 
 template <int DH, int G>
+void launch_prefill(tc_instance* I, const tc::AttnParams& p, int n_qblk, cudaStream_t s) {
+  const dim3 grid(I->d.n_kv_heads, n_qblk);
+  static const bool trace = std::getenv("TC_PF_TRACE") != nullptr;
+  if (trace) {  // tools only: %globaltimer timeline of CTA (0, 1), printed to stderr
+    tc::AttnParams q = p;
+    TC_CUDA(cudaMalloc(&q.pf_trace, 64 * 16 * 8));
+    TC_CUDA(cudaMemsetAsync(q.pf_trace, 0, 64 * 16 * 8, s));
+    launch_k(tc::attn_prefill_tc2<DH, G>, grid, tc::kPfThreads, tc::Pf2Cfg<DH, G>::kBytes, s, I->kv2_map, I->q_map, q);
+    std::vector<unsigned long long> h(64 * 16);
+    TC_CUDA(cudaMemcpyAsync(h.data(), q.pf_trace, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    cudaFree(q.pf_trace);
+    const unsigned long long t0 = h[8];
+    std::fprintf(stderr, "pf_trace (ns): key tile j | P written by softmax warps 0-7 | S seen by warps 0-7\n");
+    for (int j = 0; j < 64; ++j) {
+      if (!h[j * 16 + 8]) break;
+      std::fprintf(stderr, "pf_trace %3d", j);
+      for (int k = 0; k < 16; ++k) std::fprintf(stderr, " %6lld", h[j * 16 + k] ? (long long)(h[j * 16 + k] - t0) : -1ll);
+      std::fprintf(stderr, "\n");
+    }
+    return;
+  }
+  launch_k(tc::attn_prefill_tc2<DH, G>, grid, tc::kPfThreads, tc::Pf2Cfg<DH, G>::kBytes, s, I->kv2_map, I->q_map, p);
+}
+
+template <int DH, int G>
 void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n_dec, int dec_grid) {
-  const int hk = I->d.n_kv_heads;
   if (n_qblk > 0 && n_dec > 0 && I->pf_sms > 0) {
     // decode on the main stream over sms - pf_sms CTAs (launched first, so its persistent CTAs
     // take their SMs), prefill beside it on stream_pf over whatever SMs remain; join before O
     TC_CUDA(cudaEventRecord(I->ev_fork, I->stream));
     launch_decode<DH, G>(I, p, dec_grid);
     TC_CUDA(cudaStreamWaitEvent(I->stream_pf, I->ev_fork, 0));
-    launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream_pf,
-             I->kv2_map, I->q_map, p);
+    launch_prefill<DH, G>(I, p, n_qblk, I->stream_pf);
     TC_CUDA(cudaEventRecord(I->ev_join, I->stream_pf));
     TC_CUDA(cudaStreamWaitEvent(I->stream, I->ev_join, 0));
     I->launches += 2;
@@ -1030,8 +1054,7 @@ void launch_attention(tc_instance* I, const tc::AttnParams& p, int n_qblk, int n
     return;
   }
   if (n_qblk > 0) {
-    launch_k(tc::attn_prefill_tc<DH, G>, dim3(hk, n_qblk), tc::kPfThreads, tc::PfCfg<DH, G>::kBytes, I->stream,
-             I->kv2_map, I->q_map, p);
+    launch_prefill<DH, G>(I, p, n_qblk, I->stream);
     ++I->launches;
   }
   if (n_dec > 0) {
@@ -1086,7 +1109,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     if (EvPtr e = inbound_pending(I, st->decode[i].req_id)) waits.push_back(e);
 
   const int G = m.n_heads / m.n_kv_heads;
-  const int tpc = 128 / G;  // prefill tokens per attention CTA (one 128-row q tile)
+  const int tpc = 2 * (128 / G);  // prefill tokens per attention CTA (two 128-row q tiles)
   int n_qblk = 0, n_logit = 0, n_bt = 0;
   for (int i = 0; i < n_pf; ++i) {
     n_qblk += (st->prefill[i].n_tokens + tpc - 1) / tpc;
@@ -1102,10 +1125,10 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   for (int i = 0; i < n_dec; ++i) W += (long long)(st->decode[i].pos / ps + 1) * m.n_kv_heads;
   // Mixed steps run prefill attention beside decode attention (pf_sms SMs left to prefill; the
   // prefill CTAs spill onto every SM once the persistent decode CTAs finish). Model: decode moves
-  // its K/V at ~40 GB/s per SM up to ~5.2 TB/s; prefill costs ~2.5 us per 128-key tile + 4 us per CTA;
+  // its K/V at ~50 GB/s per SM up to ~5.6 TB/s; prefill costs ~3 us per 128-key tile + 8 us per CTA;
   // step attention time(P) = T_dec(sms - P) + max(0, W_pf - P * T_dec) / sms. The curve is flat
-  // near its minimum; take the smallest P within 0.5% of it, plus 4 (measured optima: Llama-3-8B
-  // P=512 over 512 + 64 decodes @1k: 32-40, flat; Qwen2.5-14B 1024 over 4096 + 32 @8k: 24).
+  // near its minimum; take the smallest P within 0.5% of it, plus 4 (measured optima, round 2:
+  // Llama-3-8B P=512 over 512 + 64 decodes @1k: 32-48; Qwen2.5-14B 1024 over 4096 + 32 @8k: 24-56, flat).
   // TC_PF_SMS overrides (0 = serial).
   I->pf_sms = 0;
   if (n_dec > 0 && n_qblk > 0) {
@@ -1115,12 +1138,13 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
       for (int q = 0; q < sl.n_tokens; q += tpc) pf_tiles += (sl.pos0 + std::min(q + tpc, sl.n_tokens) + 127) / 128;
     }
     pf_tiles *= m.n_kv_heads;
-    // CTA-us: ~2.5 us per 128-key tile plus ~4 us fixed per CTA (Q load, TMEM, epilogue)
-    const double w_pf = (2.5 * (double)pf_tiles + 4.0 * n_qblk * m.n_kv_heads) * (m.head_dim / 128.0);
+    // CTA-us: ~3 us per 128-key tile (both q tiles of attn_prefill_tc2; measured 2.3-2.8 us in the
+    // %globaltimer trace, TC_PF_TRACE) plus ~8 us fixed per CTA (Q load, TMEM, epilogue, tail)
+    const double w_pf = (3.0 * (double)pf_tiles + 8.0 * n_qblk * m.n_kv_heads) * (m.head_dim / 128.0);
     const double dec_bytes = (double)W * ps * m.head_dim * 2 * 2;
     // decode page-stream rate per SM and its HBM cap (bytes per us); TC_DEC_RATE="per_sm:cap" (GB/s)
     static const std::pair<double, double> dec_rate = [] {
-      double a = 40.0, b = 5200.0;
+      double a = 50.0, b = 5600.0;  // (4 producer warps: 5.6 TB/s on 124 SMs, ncu)
       if (const char* e = std::getenv("TC_DEC_RATE")) std::sscanf(e, "%lf:%lf", &a, &b);
       return std::make_pair(a * 1e3, b * 1e3);
     }();
@@ -1328,6 +1352,7 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   ap.ws_o = I->attn_ws_o;
   ap.dec_cnt = I->attn_cnt;
   ap.ws_ml = I->attn_ws_ml;
+  ap.pf_trace = nullptr;
   tc::QkvRopeArgs rp{};
   rp.kv = I->kv;
   rp.rope_cs = I->rope;
