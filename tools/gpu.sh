@@ -42,8 +42,9 @@ for st in ${STAGES:-tests smoke bench}; do
           > gpurun_out/san_${tool}_$TAG.txt 2>&1; echo "$tool rc=$?"; tail -3 gpurun_out/san_${tool}_$TAG.txt
       done ;;
     ab) for v in ${VARIANTS}; do
-        env ${v//,/ } timeout 600 $B ${BENCH_ARGS} > gpurun_out/ab_${TAG}_${v//[=,]/_}.json 2>&1
-        echo "$v: $(python3 -c "import json,sys; j=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(round(j['value']), round(j['ms_per_step'],3), j.get('decode_only_step',{}) and round(j['decode_only_step']['ms'],3))" gpurun_out/ab_${TAG}_${v//[=,]/_}.json 2>&1 | tail -1)"
+        n=$(echo "$v" | tr '=,/' '___')
+        env ${v//,/ } timeout 600 $B ${BENCH_ARGS} > gpurun_out/ab_${TAG}_$n.json 2>&1
+        echo "$v: $(python3 -c "import json,sys; j=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(round(j['value']), round(j['ms_per_step'],3), j.get('decode_only_step',{}) and round(j['decode_only_step']['ms'],3))" gpurun_out/ab_${TAG}_$n.json 2>&1 | tail -1)"
       done ;;
     cmd) bash -c "$CMD" ;;
   esac
