@@ -8,6 +8,9 @@
 #   prof      ncu --set full of the step kernels ($PROF_K regex, default all step kernels)
 #   san       compute-sanitizer racecheck / synccheck / memcheck on smoke()
 #   ab        $VARIANTS (space-separated env assignments, comma-joined within one variant) on bench
+#   calib     cost-model calibration on the current kernels -> gpurun_out/b200_calibration_$MODEL_$TAG.json
+#   goodput   device-clock SLO goodput: GP_BASE config, GP_MODES, GP_QPS, GP_SEEDS (default 0,1,2), GP_SLO
+#             (TTFT_ms,TPOT_ms override), GP_MODEL, GP_PROFILE (calibration JSON) -> gpurun_out/goodput_$TAG.json
 #   cmd       $CMD (free-form)
 cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"; mkdir -p gpurun_out; export PYTHONUNBUFFERED=1
 TAG=${TAG:-x}
@@ -46,6 +49,11 @@ for st in ${STAGES:-tests smoke bench}; do
         env ${v//,/ } timeout 600 $B ${BENCH_ARGS} > gpurun_out/ab_${TAG}_$n.json 2>&1
         echo "$v: $(python3 -c "import json,sys; j=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(round(j['value']), round(j['ms_per_step'],3), j.get('decode_only_step',{}) and round(j['decode_only_step']['ms'],3))" gpurun_out/ab_${TAG}_$n.json 2>&1 | tail -1)"
       done ;;
+    calib) timeout 1200 python tools/calibrate.py --model ${MODEL:-llama3_8b} --out gpurun_out/b200_calibration_${MODEL:-llama3_8b}_$TAG.json 2>&1 | tail -3 ;;
+    goodput) timeout ${GP_TIMEOUT:-3600} python tools/goodput.py --base ${GP_BASE:-configs/b200_c3_4p4d.json} \
+        --modes ${GP_MODES:-hybrid,aggregation,disaggregation} --qps ${GP_QPS} --seeds ${GP_SEEDS:-0,1,2} \
+        --model ${GP_MODEL:-llama3_8b} ${GP_PROFILE:+--profile $GP_PROFILE} ${GP_SLO:+--slo $GP_SLO} ${GP_ARGS} \
+        --out gpurun_out/goodput_$TAG.json > gpurun_out/goodput_$TAG.txt 2>&1; grep GOODPUT gpurun_out/goodput_$TAG.txt ;;
     cmd) bash -c "$CMD" ;;
   esac
 done
