@@ -170,34 +170,44 @@ __global__ void __launch_bounds__(THREADS) argmax_rows(const float* __restrict__
 }
 
 // ---------------------------------------------------------------- KV migration
-// Copies whole pages (all layers) of one request: dst_pool[dst_pages[i]] = src_pool[src_pages[i]].
-// Pools may live on different GPUs (peer pointers over NVLink, UVA); one
-// launch moves every page of the request with 16 B loads, several in flight per thread.
-__global__ void __launch_bounds__(512) kv_copy_pages(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
-                                                     const int* __restrict__ src_pages, const int* __restrict__ dst_pages,
-                                                     int n_pages, long long page_vec) {
-  const long long total = (long long)n_pages * page_vec;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  constexpr int U = 4;
-  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total; base += stride * U) {
-    uint4 v[U];
+// Whole-page copies of one request's KV (all layers): dst_pool[dst_page[i]] = src_pool[src_page[i]].
+// Pools may live on different GPUs (peer pointers over NVLink, UVA). Work unit = one 64 KiB slice
+// of a page per block iteration (512 threads x 8 x 16 B loads in flight, then the stores): 32-bit
+// index math once per slice (round 1 divided a 64-bit element index by the page size per 16 B).
+constexpr int kCopyThreads = 512;
+constexpr int kCopySliceVec = kCopyThreads * 8;  // 16 B vectors per slice (64 KiB)
+
+template <typename SrcPage, typename DstPage>
+__device__ __forceinline__ void copy_page_slices(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
+                                                 SrcPage&& src_page, DstPage&& dst_page, int n_pages, long long page_vec) {
+  const int spp = (int)((page_vec + kCopySliceVec - 1) / kCopySliceVec);  // slices per page
+  for (int b = blockIdx.x; b < n_pages * spp; b += gridDim.x) {
+    const int pg = b / spp;
+    const long long off = (long long)(b - pg * spp) * kCopySliceVec;
+    const uint4* s = src_pool + (long long)src_page(pg) * page_vec + off;
+    uint4* d = dst_pool + (long long)dst_page(pg) * page_vec + off;
+    const int n = (int)min((long long)kCopySliceVec, page_vec - off);
+    uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < total) {
-        const long long pg = i / page_vec, off = i % page_vec;
-        v[u] = ld_nc_v4(src_pool + (long long)src_pages[pg] * page_vec + off);
-      }
+    for (int u = 0; u < 8; ++u) {
+      const int i = threadIdx.x + u * kCopyThreads;
+      if (i < n) v[u] = ld_nc_v4(s + i);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < total) {
-        const long long pg = i / page_vec, off = i % page_vec;
-        st_global_v4(dst_pool + (long long)dst_pages[pg] * page_vec + off, v[u]);
-      }
+    for (int u = 0; u < 8; ++u) {
+      const int i = threadIdx.x + u * kCopyThreads;
+      if (i < n) st_global_v4(d + i, v[u]);
     }
   }
+}
+
+// page lists in device memory (tc_copy_pages)
+__global__ void __launch_bounds__(kCopyThreads) kv_copy_pages(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
+                                                              const int* __restrict__ src_pages,
+                                                              const int* __restrict__ dst_pages, int n_pages,
+                                                              long long page_vec) {
+  copy_page_slices(src_pool, dst_pool, [&](int i) { return src_pages[i]; }, [&](int i) { return dst_pages[i]; }, n_pages,
+                   page_vec);
 }
 
 // Page lists of one asynchronous migration travel in the kernel's parameter space (16 KB of the
@@ -210,30 +220,9 @@ struct MigPages {
   int32_t dst[kMigPagesPerLaunch];
 };
 
-__global__ void __launch_bounds__(512) kv_migrate_pages(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
-                                                        const __grid_constant__ MigPages pl, long long page_vec) {
-  const long long total = (long long)pl.n * page_vec;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  constexpr int U = 4;
-  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total; base += stride * U) {
-    uint4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < total) {
-        const int pg = (int)(i / page_vec);
-        v[u] = ld_nc_v4(src_pool + (long long)pl.src[pg] * page_vec + (i - (long long)pg * page_vec));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < total) {
-        const int pg = (int)(i / page_vec);
-        st_global_v4(dst_pool + (long long)pl.dst[pg] * page_vec + (i - (long long)pg * page_vec), v[u]);
-      }
-    }
-  }
+__global__ void __launch_bounds__(kCopyThreads) kv_migrate_pages(const uint4* __restrict__ src_pool, uint4* __restrict__ dst_pool,
+                                                                 const __grid_constant__ MigPages pl, long long page_vec) {
+  copy_page_slices(src_pool, dst_pool, [&](int i) { return pl.src[i]; }, [&](int i) { return pl.dst[i]; }, pl.n, page_vec);
 }
 
 }  // namespace tc

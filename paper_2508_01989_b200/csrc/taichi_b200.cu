@@ -1545,7 +1545,7 @@ tc_event* launch_page_copy(tc_instance* src, const void* dst_key, void* dst_base
   if (after) TC_CUDA(cudaStreamWaitEvent(cs, after, 0));
   TC_CUDA(cudaEventRecord(ev->t0, cs));
   const int64_t page_vec = src->page_elems * 2 / 16;
-  const int cap = src->mig_ctas > 0 ? src->mig_ctas : 2 * src->sms;
+  const int cap = src->mig_ctas > 0 ? src->mig_ctas : 4 * src->sms;
   for (int64_t b0 = 0; b0 < np; b0 += tc::kMigPagesPerLaunch) {
     tc::MigPages pl;
     pl.n = (int)std::min<int64_t>(tc::kMigPagesPerLaunch, np - b0);
@@ -1553,8 +1553,9 @@ tc_event* launch_page_copy(tc_instance* src, const void* dst_key, void* dst_base
       pl.src[i] = sp[b0 + i];
       pl.dst[i] = dp[b0 + i];
     }
-    const int blocks = (int)std::min<int64_t>(cap, std::max<int64_t>(1, pl.n * page_vec / (512 * 4)));
-    tc::kv_migrate_pages<<<blocks, 512, 0, cs>>>(reinterpret_cast<const uint4*>(src->kv), reinterpret_cast<uint4*>(dst_base),
+    const int64_t slices = (int64_t)pl.n * ((page_vec + tc::kCopySliceVec - 1) / tc::kCopySliceVec);
+    const int blocks = (int)std::min<int64_t>(cap, std::max<int64_t>(1, slices));
+    tc::kv_migrate_pages<<<blocks, tc::kCopyThreads, 0, cs>>>(reinterpret_cast<const uint4*>(src->kv), reinterpret_cast<uint4*>(dst_base),
                                                  pl, page_vec);
     TC_CUDA(cudaGetLastError());
   }
@@ -1703,10 +1704,12 @@ tc_status tc_instance_create(const tc_instance_desc* desc, tc_instance** out) {
       I->pool->page_elems = I->page_elems;
       int64_t tokens = desc->kv_pool_tokens;
       if (tokens <= 0) {
-        // auto: every free byte of HBM but a 4 GiB reserve (production sizing)
+        // auto: every free byte of HBM but a reserve of max(4 GiB, 12% of HBM) -- room for the step
+        // workspaces (~0.8 GB each at Llama-3-8B) of up to ~20 instances that share this GPU and
+        // this pool (share_kv_pool), e.g. the 8 instances of config 3 time-shared on one B200
         size_t free_b = 0, total_b = 0;
         TC_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const int64_t usable = (int64_t)free_b - ((int64_t)4 << 30);
+        const int64_t usable = (int64_t)free_b - std::max<int64_t>((int64_t)4 << 30, (int64_t)(0.12 * (double)total_b));
         TC_REQUIRE(usable > I->page_elems * 2, "create: no HBM left for a KV pool");
         tokens = usable / (I->page_elems * 2) * desc->page_size;
       }
@@ -1985,8 +1988,9 @@ tc_status tc_copy_pages(const void* src_pool, void* dst_pool, const int32_t* src
     TC_CUDA(cudaGetDevice(&dev));
     const int sms = device_sms(dev);
     const int64_t page_vec = page_bytes / 16;
-    const int blocks = (int)std::min<int64_t>(2 * sms, std::max<int64_t>(1, n_pages * page_vec / (512 * 4)));
-    tc::kv_copy_pages<<<blocks, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+    const int64_t slices = (int64_t)n_pages * ((page_vec + tc::kCopySliceVec - 1) / tc::kCopySliceVec);
+    const int blocks = (int)std::min<int64_t>(4 * sms, std::max<int64_t>(1, slices));
+    tc::kv_copy_pages<<<blocks, tc::kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const uint4*>(src_pool), reinterpret_cast<uint4*>(dst_pool), src_pages_dev, dst_pages_dev,
         n_pages, page_vec);
     TC_CUDA(cudaGetLastError());

@@ -101,7 +101,7 @@ int main(int argc, char** argv) {
       // The logical kv_capacity (cluster.hpp:130-181) only counts resident decodes; the physical pool
       // must also hold in-flight prefills, pending decodes (Init transfers are admitted without a
       // fit check, engine.hpp:512) and KV in transit. One pool per GPU, shared by the instances on
-      // it: --pool-tokens, default every free byte of HBM but 4 GiB (SURVEY App. B sizing).
+      // it: --pool-tokens, default every free byte of HBM but max(4 GiB, 12%) (SURVEY App. B sizing).
       d.kv_pool_tokens = pool_tokens > 0 ? pool_tokens : 0;
       d.max_step_tokens = static_cast<int32_t>(std::max<Tokens>(sp.chunk_size, 1) + 1024);
       d.max_seqs = 1024;
