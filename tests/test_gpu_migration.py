@@ -147,3 +147,23 @@ def test_cross_gpu_migration_over_nvlink(model):
     f.check(int(o2.sampled[0]), o2.logits[0])
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("page_bytes,n_pages", [(2 << 20, 37), (3 << 20, 5), (16 * 2 * 2 * 64 * 2, 300), (65536 + 4096, 9)])
+def test_copy_pages_kernel_bytes(page_bytes, n_pages):
+    """K11's copy kernel (tc_copy_pages, the same slice loop as the migration kernel) moves whole
+    pages byte-exactly for page sizes that are, and are not, multiples of its 64 KiB slice."""
+    from paper_2508_01989_b200 import runtime
+    g = torch.Generator(device="cpu").manual_seed(page_bytes + n_pages)
+    pool_pages = 2 * n_pages + 3
+    src = torch.randint(-2**31, 2**31 - 1, (pool_pages, page_bytes // 4), generator=g, dtype=torch.int32).cuda()
+    dst = torch.zeros_like(src)
+    sp = torch.randperm(pool_pages, generator=g)[:n_pages].to(torch.int32)
+    dp = torch.randperm(pool_pages, generator=g)[:n_pages].to(torch.int32)
+    spd, dpd = sp.cuda(), dp.cuda()
+    runtime.copy_pages(src.data_ptr(), dst.data_ptr(), spd.data_ptr(), dpd.data_ptr(), n_pages, page_bytes,
+                       torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = torch.zeros_like(src)
+    ref[dp.long().cuda()] = src[sp.long().cuda()]
+    assert torch.equal(dst, ref)
