@@ -648,11 +648,22 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
         sa = p.dec_seg_a[ent.x];
       }
       const int ne = min(32, e_end - e0);
+      // lane j: block-table entry of page c + j of the chunk being issued. Loaded one chunk ahead --
+      // the next chunk of this entry, or the first chunk of the next entry -- so the global-load
+      // latency stays off the issue path (round 1 stalled the stream on it at every entry)
+      auto first_chunk = [&](int k) {
+        const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
+        const int bt_off = __shfl_sync(0xffffffffu, sa.x, k);
+        return pg0 + lane < pg1 ? __ldg(p.block_tables + bt_off + pg0 + lane) : 0;
+      };
+      int bt_first = first_chunk(0);
       for (int k = 0; k < ne; ++k) {
         const int e = e0 + k - e_begin;  // local entry index
         const int pg0 = __shfl_sync(0xffffffffu, ent.y, k), pg1 = __shfl_sync(0xffffffffu, ent.z, k);
         const int bt_off = __shfl_sync(0xffffffffu, sa.x, k), q_row = __shfl_sync(0xffffffffu, sa.z, k);
         const int kvh = __shfl_sync(0xffffffffu, sa.w, k);
+        int bt_next = bt_first;
+        if (k + 1 < ne) bt_first = first_chunk(k + 1);
         if (lane == 0 && pj == 0) {
           const int b = e & 1;
           mbar_wait(&qempty[b], ((e >> 1) & 1) ^ 1);
@@ -661,8 +672,8 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
                     p.qkv + (long long)q_row * qkv_ld + kvh * G * DH, SM::kQBytes, &qfull[b]);
         }
         for (int c = pg0; c < pg1; c += 32) {
-          // lane j: pool row of page c + j (coordinates computed 32 at a time, off the issue path)
-          const int row = c + lane < pg1 ? kv_row(p, p.block_tables[bt_off + c + lane], kvh) : 0;
+          const int row = c + lane < pg1 ? kv_row(p, bt_next, kvh) : 0;
+          if (c + 32 + lane < pg1) bt_next = __ldg(p.block_tables + bt_off + c + 32 + lane);
           const int n = min(32, pg1 - c);
           for (int j = 0; j < n; ++j, ++g) {
             const int rj = __shfl_sync(0xffffffffu, row, j);
