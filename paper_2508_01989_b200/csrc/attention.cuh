@@ -618,9 +618,11 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&qfull[b], 1);
-      mbar_init(&qempty[b], NC);
-      mbar_init(&pfull[b], NC);
-      mbar_init(&pempty[b], 1);
+      // every lane arrives on the hand-off barriers, so each lane's own shared-memory accesses are
+      // ordered by its own arrival (compute-sanitizer racecheck clean)
+      mbar_init(&qempty[b], NC * 32);
+      mbar_init(&pfull[b], NC * 32);
+      mbar_init(&pempty[b], 32);
     }
     mbar_fence_init();
   }
@@ -719,7 +721,7 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
             },
             acc, mm, ll);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pempty[b]);  // buffer b free for entry e + 2
+        mbar_arrive(&pempty[b]);  // buffer b free for entry e + 2
         __nv_bfloat16* out_row = p.out + (long long)q_row * p.n_heads * DH + (long long)kvh * G * DH;
         if (n_parts == 1) {
           store_out_row<DH, G>(out_row, acc, ll);
@@ -793,7 +795,7 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&qempty[b]);
+      mbar_arrive(&qempty[b]);
       float o[DH / 16][4];
 #pragma unroll
       for (int mt = 0; mt < DH / 16; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
@@ -830,7 +832,7 @@ __global__ void __launch_bounds__(dec_threads(NC, NP), 1) attn_decode(const __gr
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[b]);  // release: the partial's stores precede the arrival
+      mbar_arrive(&pfull[b]);  // release: the partial's stores precede the arrival
     }
   }
 }
