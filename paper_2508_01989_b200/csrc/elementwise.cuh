@@ -68,13 +68,10 @@ __global__ void embed_rows(const int* __restrict__ tokens, const __nv_bfloat16* 
 // out[r, :] = bf16(x[src_row(r), :] * rsqrt(mean(x^2) + eps) * w), fp32 math.
 // rows == nullptr: identity row map; otherwise gathers rows (sampled-row LM head).
 // The row is read once into registers (<= kMaxVec float4 per thread: d <= 8192).
-// zero / zero_cols (optional): also clear row r of an fp32 scratch that the next GEMM
-// accumulates into with red.add (decode-only streaming mode), saving a memset launch.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict__ x, const int* __restrict__ rows,
                                                         const __nv_bfloat16* __restrict__ w,
-                                                        __nv_bfloat16* __restrict__ out, int d, float eps,
-                                                        float* __restrict__ zero = nullptr, int zero_cols = 0) {
+                                                        __nv_bfloat16* __restrict__ out, int d, float eps) {
   constexpr int kMaxVec = 8192 / (4 * THREADS);
   // the norm weights do not depend on the predecessor kernel: fetch them before the PDL wait
   uint2 wv[kMaxVec];
@@ -117,10 +114,6 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_rows(const float* __restrict_
       pk.y = pack_bf16(v[i].z * inv * w23.x, v[i].w * inv * w23.y);
       *reinterpret_cast<uint2*>(o + c) = pk;
     }
-  }
-  if (zero) {
-    float4* z = reinterpret_cast<float4*>(zero + (long long)r * zero_cols);
-    for (int c = threadIdx.x; c < zero_cols / 4; c += THREADS) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 

@@ -79,8 +79,6 @@ struct GemmArgs {
   float* ws;                 // partial slots [units][BN/32][128][32] (splits > 1)
   int* tile_cnt;             // per-tile arrival counters (zero; last arriver resets)
   QkvRopeArgs rope;          // EPI_QKV_ROPE only
-  float* red_out;            // small-M streaming mode: every unit red.adds its partial into this
-                             // zeroed fp32 [M, N] scratch; a finish kernel applies the epilogue
   int tn;                    // gemm_ws_2sm: token tile (multiple of 32, <= 256)
   int stages;                // gemm_ws_2sm: smem ring depth for this token tile
   unsigned long long* trace; // gemm_ws_2sm (tools only): per-CTA %globaltimer stamps [grid][16]
@@ -374,26 +372,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m = mt * kGemmBM + row;
       const bool row_ok = m < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-      if (args.red_out != nullptr) {  // streaming mode (decode-only steps): accumulate and move on
-#pragma unroll 1
-        for (int chunk = 0; chunk < BN / 32; ++chunk) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + chunk * 32, r);
-          tmem_ld_wait();
-          if (row_ok) {
-            float* dst = args.red_out + (size_t)m * args.N + nt * BN + chunk * 32;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + q * 4),
-                           "f"(__uint_as_float(r[q * 4])), "f"(__uint_as_float(r[q * 4 + 1])),
-                           "f"(__uint_as_float(r[q * 4 + 2])), "f"(__uint_as_float(r[q * 4 + 3]))
-                           : "memory");
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty_bar[acc]);
-        continue;
-      }
       // residual-add GEMMs reduce split-K partials with red.global.add (no workspace)
       const bool whole = args.splits == 1 || EPI == EPI_RESID_F32;
 
@@ -515,98 +493,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
-  }
-}
-
-// ---------------------------------------------------------------- streaming-mode finishers
-// SwiGLU over the fp32 scratch of a 64-interleaved gate|up GEMM: act[m, j] = silu(g) * u.
-// Each finisher zeroes the scratch it consumed, so the next streaming GEMM can accumulate into it
-// without a separate clearing pass (the scratch is zeroed once at instance creation).
-__global__ void finish_swiglu(float* __restrict__ scr, int M, int F, __nv_bfloat16* __restrict__ act) {
-  pdl_wait();
-  pdl_trigger();
-  // grid (column blocks, rows): no 64-bit division in the index math (it dominated: 22 us per
-  // layer at 64 rows x 14336)
-  const int m = blockIdx.y;
-  float* row = scr + (size_t)m * 2 * F;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
-    const int gc = ((j >> 6) << 7) + (j & 63);
-    const float4 g = *reinterpret_cast<const float4*>(row + gc);
-    const float4 u = *reinterpret_cast<const float4*>(row + gc + 64);
-    *reinterpret_cast<float4*>(row + gc) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(row + gc + 64) = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint2 w;
-    w.x = pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y);
-    w.y = pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w);
-    *reinterpret_cast<uint2*>(act + (size_t)m * F + j) = w;
-  }
-}
-
-// (+bias) -> RoPE(q, k) -> q into q_out, k / v into the paged pool; one thread per
-// (row, head, rotation pair j < head_dim / 2).
-__global__ void finish_qkv_rope(float* __restrict__ scr, int M, QkvRopeArgs r, const __nv_bfloat16* bias,
-                                __nv_bfloat16* __restrict__ q_out, int q_ld) {
-  pdl_wait();
-  pdl_trigger();
-  // one thread per (row, head, 8 consecutive rotation pairs): 16 B vector loads / stores
-  const int half = r.head_dim / 2, groups = half / 8;
-  const int heads = r.n_heads + 2 * r.n_kv_heads;
-  const int N = heads * r.head_dim;
-  // grid (blocks over heads x groups, rows): 32-bit index math only
-  const int m = blockIdx.y;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < heads * groups; i += gridDim.x * blockDim.x) {
-    const int j0 = (i % groups) * 8;
-    const int head = i / groups;
-    const int c = head * r.head_dim + j0;
-    float* srow = scr + (size_t)m * N;
-    float lo[8], hi[8];
-    {
-      const float4 a0 = *reinterpret_cast<const float4*>(srow + c), a1 = *reinterpret_cast<const float4*>(srow + c + 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(srow + c + half);
-      const float4 b1 = *reinterpret_cast<const float4*>(srow + c + half + 4);
-      lo[0] = a0.x; lo[1] = a0.y; lo[2] = a0.z; lo[3] = a0.w; lo[4] = a1.x; lo[5] = a1.y; lo[6] = a1.z; lo[7] = a1.w;
-      hi[0] = b0.x; hi[1] = b0.y; hi[2] = b0.z; hi[3] = b0.w; hi[4] = b1.x; hi[5] = b1.y; hi[6] = b1.z; hi[7] = b1.w;
-      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(srow + c) = z;
-      *reinterpret_cast<float4*>(srow + c + 4) = z;
-      *reinterpret_cast<float4*>(srow + c + half) = z;
-      *reinterpret_cast<float4*>(srow + c + half + 4) = z;
-    }
-    if (bias) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        lo[e] += __bfloat162float(bias[c + e]);
-        hi[e] += __bfloat162float(bias[c + half + e]);
-      }
-    }
-    const int pos = r.positions[m];
-    const bool is_q = head < r.n_heads, is_k = !is_q && head < r.n_heads + r.n_kv_heads;
-    if (is_q || is_k) {
-      const float4* cs = reinterpret_cast<const float4*>(r.rope_cs + (size_t)pos * half + j0);
-#pragma unroll
-      for (int e = 0; e < 8; e += 2) {
-        const float4 t = cs[e / 2];  // (cos, sin) x 2
-        const float a0 = lo[e], b0 = hi[e], a1 = lo[e + 1], b1 = hi[e + 1];
-        lo[e] = a0 * t.x - b0 * t.y;
-        hi[e] = b0 * t.x + a0 * t.y;
-        lo[e + 1] = a1 * t.z - b1 * t.w;
-        hi[e + 1] = b1 * t.z + a1 * t.w;
-      }
-    }
-    __nv_bfloat16* dst;
-    if (is_q) {
-      dst = q_out + (size_t)m * q_ld + head * r.head_dim;
-    } else {
-      const int kv_row = r.row_kv[m];
-      const int page = kv_row / r.page_size, slot = kv_row - page * r.page_size;
-      const int kvh = head - r.n_heads - (is_k ? 0 : r.n_kv_heads);
-      dst = r.kv + (size_t)page * r.page_stride +
-            ((((size_t)r.layer * r.n_kv_heads + kvh) * 2 + (is_k ? 0 : 1)) * r.page_size + slot) * r.head_dim;
-    }
-    st_global_v4(dst + j0, make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
-                                      pack_bf16(lo[6], lo[7])));
-    st_global_v4(dst + j0 + half, make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
-                                             pack_bf16(hi[6], hi[7])));
   }
 }
 

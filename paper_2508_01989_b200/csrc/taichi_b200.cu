@@ -215,32 +215,12 @@ struct GemmChoice {
 //  * M > 128 (mixed / prefill steps): data-parallel 128x256 tiles. Split-K loses at M = 576
 //    (down: 98 us unsplit vs 125 us with 3 splits) because the partial round trip and the
 //    last-arriver reduction land in the tail of the wave.
-//  * M <= 128 (decode-only steps, weight streaming): 128-wide tiles split 3 ways when fewer
-//    than half the SMs would get a tile (qkv 23 -> 21 us, down 66 -> 41 us at M = 64).
-GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits, bool streaming = false) {
+//  * M <= 128: 128-wide tiles split 3 ways when fewer than half the SMs would get a tile
+//    (qkv 23 -> 21 us, down 66 -> 41 us at M = 64).
+GemmChoice choose_gemm(int M, int N, int K, int epi, int sms, int force_bn, int force_splits) {
   GemmChoice c{};
   c.m_tiles = (M + tc::kGemmBM - 1) / tc::kGemmBM;
   c.kb = K / tc::kGemmBK;
-  if (streaming && !force_bn && !force_splits) {
-    // decode-only steps (M <= 128): the GEMM is a weight stream. Pick splits so every SM streams
-    // (~40 GB/s per SM) with few waves: t = weight bytes / (active SMs * 40 GB/s) + 2 us per wave.
-    c.bn = (N % 256 == 0) ? 256 : 128;
-    c.n_tiles = N / c.bn;
-    const long long tiles = (long long)c.m_tiles * c.n_tiles;
-    double best = 1e30;
-    for (int sp = 1; sp <= std::min(16, std::max(1, c.kb / 4)); ++sp) {
-      const long long units = tiles * sp, active = std::min<long long>(units, sms);
-      const long long waves = (units + sms - 1) / sms;
-      const double t = (double)N * K * 2 / (active * 40.0e3) + 2.0 * waves;
-      if (t < best - 1e-9) {
-        best = t;
-        c.splits = sp;
-      }
-    }
-    c.grid = (int)std::min<long long>(sms, tiles * c.splits);
-    c.est_us = best;
-    return c;
-  }
   if (force_bn) c.bn = force_bn;
   else if (epi != tc::EPI_RESID_F32 && M <= tc::kGemmBM && (long long)c.m_tiles * (N / 128) < sms / 2) c.bn = 128;
   else c.bn = (N % 256 == 0) ? 256 : 128;
@@ -373,7 +353,7 @@ tc::GemmArgs plan_gemm_ws(int M, int N, int K, int epi, int sms, int force_split
   args.kb = K / tc::kGemmBK;
   const long long tiles = (long long)args.m_tiles * args.n_tiles;
   const int pairs = sms / 2;
-  // Residual epilogue (O / down, and the decode-only streaming scratch): every partial is a TMA
+  // Residual epilogue (O / down): every partial is a TMA
   // bulk add, so the k-blocks are spread by GROUPED stream-K -- pair groups of n_tt siblings (one
   // per token tile) walk the weight-tile-major (tile, k-block) stream in lockstep, group g taking
   // [W g / G, W (g+1) / G) (W = weight tiles * kb), cut at tile boundaries. Every pair gets the same
@@ -475,7 +455,7 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
 // out = epi(A[M,K] * W[N,K]^T). a: the activation buffer's maps.
 int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfloat16* bias, int epi,
              int sms, const SkWorkspace& sk, cudaStream_t s, int force_bn = 0, int force_splits = 0,
-             const tc::QkvRopeArgs* rope = nullptr, float* red_out = nullptr, const CUtensorMap* out_map = nullptr) {
+             const tc::QkvRopeArgs* rope = nullptr, const CUtensorMap* out_map = nullptr) {
   const int N = (int)w.rows, K = (int)w.cols;
   TC_REQUIRE(K % 64 == 0, "gemm: K must be a multiple of 64");
   TC_REQUIRE(N % 128 == 0, "gemm: N must be a multiple of 128");
@@ -487,14 +467,10 @@ int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfl
   }();
   if (N % 256 == 0 &&
       (force_bn == 1024 || (force_bn == 0 && ws_enabled() && epi != tc::EPI_F32 && (M > kWsMinRows || ws_small)))) {
-    // streaming mode (decode-only steps): split-K partials land in the zeroed fp32 scratch via
-    // TMA bulk adds; the finish kernel applies RoPE + KV append / SwiGLU
-    if (red_out != nullptr) return run_gemm_ws(a, w, M, red_out, N, nullptr, tc::EPI_RESID_F32, sms, s, force_splits,
-                                               nullptr, nullptr);
     return run_gemm_ws(a, w, M, out, ldo, bias, epi, sms, s, force_splits, rope, out_map);
   }
   const CUtensorMap& a_map = a.m128;
-  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits, red_out != nullptr);
+  const GemmChoice c = choose_gemm(M, N, K, epi, sms, force_bn, force_splits);
   TC_REQUIRE((long long)c.m_tiles * c.n_tiles <= kSkMaxTiles, "gemm: too many tiles");
   tc::GemmArgs args{};
   args.M = M;
@@ -510,8 +486,7 @@ int run_gemm(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_bfl
   args.bias = bias;
   args.ws = sk.ws;
   args.tile_cnt = sk.cnt;
-  args.red_out = red_out;
-  if (epi == tc::EPI_QKV_ROPE && red_out == nullptr) {
+  if (epi == tc::EPI_QKV_ROPE) {
     TC_REQUIRE(rope != nullptr, "gemm: fused QKV epilogue needs RoPE / KV metadata");
     TC_REQUIRE(c.bn % rope->head_dim == 0, "gemm: tile width must cover whole heads");
     args.rope = *rope;
@@ -529,7 +504,6 @@ struct LayerW {
 };
 
 constexpr int kMaxDecodeItems = 16384;
-constexpr int kStreamRows = 128;  // steps with <= this many rows run their QKV / gate_up GEMMs in streaming mode
 
 constexpr uint64_t kTidEmbed = 1, kTidLmHead = 2, kTidFinalNorm = 3;
 inline uint64_t tid_layer(int l, int j) { return 16 + 16ull * l + j; }
@@ -742,7 +716,6 @@ struct tc_instance {
   ActMap map_xnorm, map_attn, map_act, map_lm_in;
   CUtensorMap map_resid;  // fp32 residual stream, target of the GEMMs' TMA bulk adds
   SkWorkspace sk;
-  float* stream_scr = nullptr;  // fp32 [<=128, max(qkv_n, 2F)] accumulation scratch (decode-only steps)
   float *attn_ws_o = nullptr, *attn_ws_ml = nullptr;
   int* attn_cnt = nullptr;
   size_t attn_ws_floats = 0;
@@ -903,9 +876,6 @@ void alloc_buffers(tc_instance* I) {
     const cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)(128 / G)};
     I->q_map = encode_map(I->qkv, 3, dims, strides, box);
   }
-  TC_CUDA(cudaMalloc(&I->stream_scr, (size_t)kStreamRows * std::max<int64_t>(I->qkv_n, 2 * (int64_t)m.ffn_dim) * 4));
-  // zero once; the finish kernels re-zero what they consume (no per-step clearing pass)
-  TC_CUDA(cudaMemset(I->stream_scr, 0, (size_t)kStreamRows * std::max<int64_t>(I->qkv_n, 2 * (int64_t)m.ffn_dim) * 4));
   // stream-K partial slots + tile counters (counters must start at zero)
   TC_CUDA(cudaMalloc(&I->sk.ws, kSkWsBytes));
   TC_CUDA(cudaMalloc(&I->sk.cnt, (size_t)kSkMaxTiles * 4));
@@ -1367,31 +1337,24 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
   rp.head_dim = m.head_dim;
   rp.page_size = ps;
   constexpr int rms_threads = 256;
-  // decode-heavy steps: QKV / gate_up stream their weights over every SM (split-K, red.add into a
-  // zeroed fp32 scratch) and a finish kernel applies RoPE + KV append / SwiGLU
-  const bool streaming = T <= kStreamRows;
+  // Every step, decode-only ones included, runs each projection as direct weight-stationary units
+  // with its fused epilogue. (Round 2 measured the alternative for T <= 128 -- stream-K partials
+  // into a zeroed fp32 scratch plus RoPE / SwiGLU finish kernels -- at 5.44 vs 5.22 ms per
+  // decode-only step: the finish kernels and the scratch round trip cost more than the direct
+  // units' 1.5-wave imbalance on gate_up and QKV's 24 busy pairs.)
   for (int l = 0; l < m.n_layers; ++l) {
     const LayerW& L = I->layers[l];
     {
       ProfScope p_(I, "norm");
-      launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps,
-                                                              (float*)nullptr, 0);
+      launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.attn_norm, I->xnorm, m.d_model, m.rms_eps);
       ++I->launches;
     }
     {
       // QKV projection with fused bias, RoPE and paged KV append (q stays in I->qkv)
       ProfScope p_(I, "gemm_qkv");
       rp.layer = l;
-      if (streaming) {
-        I->launches += run_gemm(I->map_xnorm, L.qkv, T, nullptr, I->qkv_n, nullptr, tc::EPI_BF16, I->sms, I->sk, s, 0, 0,
-                                nullptr, I->stream_scr, nullptr);
-        launch_k(tc::finish_qkv_rope, dim3((I->qkv_n / 16 + 255) / 256, T), 256, 0, s, I->stream_scr, T, rp, m.qkv_bias ? L.qkv_bias : nullptr, I->qkv,
-                                                      I->qkv_n);
-        ++I->launches;
-      } else {
-        I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
-                                tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp, nullptr, nullptr);
-      }
+      I->launches += run_gemm(I->map_xnorm, L.qkv, T, I->qkv, I->qkv_n, m.qkv_bias ? L.qkv_bias : nullptr,
+                              tc::EPI_QKV_ROPE, I->sms, I->sk, s, 0, 0, &rp, nullptr);
     }
     {
       ProfScope p_(I, "attn");
@@ -1401,36 +1364,27 @@ void step_launch(tc_instance* I, const tc_step_desc* st) {
     {
       ProfScope p_(I, "gemm_o");
       I->launches += run_gemm(I->map_attn, L.o, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
-                              nullptr, nullptr, &I->map_resid);
+                              nullptr, &I->map_resid);
     }
     {
       ProfScope p_(I, "norm");
-      launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps,
-                                                              (float*)nullptr, 0);
+      launch_k(tc::rmsnorm_rows<rms_threads>, T, rms_threads, 0, s, I->resid, nullptr, L.mlp_norm, I->xnorm, m.d_model, m.rms_eps);
       ++I->launches;
     }
     {
       ProfScope p_(I, "gemm_gate_up");
-      if (streaming) {
-        I->launches += run_gemm(I->map_xnorm, L.gate_up, T, nullptr, m.ffn_dim, nullptr, tc::EPI_BF16, I->sms, I->sk, s,
-                                0, 0, nullptr, I->stream_scr, nullptr);
-        launch_k(tc::finish_swiglu, dim3((m.ffn_dim / 4 + 255) / 256, T), 256, 0, s, I->stream_scr, T, m.ffn_dim, I->act);
-        ++I->launches;
-      } else {
-        I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s,
-                                0, 0, nullptr, nullptr, nullptr);
-      }
+      I->launches += run_gemm(I->map_xnorm, L.gate_up, T, I->act, m.ffn_dim, nullptr, tc::EPI_SWIGLU, I->sms, I->sk, s);
     }
     {
       ProfScope p_(I, "gemm_down");
       I->launches += run_gemm(I->map_act, L.down, T, I->resid, m.d_model, nullptr, tc::EPI_RESID_F32, I->sms, I->sk, s, 0, 0,
-                              nullptr, nullptr, &I->map_resid);
+                              nullptr, &I->map_resid);
     }
   }
   if (n_logit > 0) {
     ProfScope p_(I, "lm_head");
     launch_k(tc::rmsnorm_rows<rms_threads>, n_logit, rms_threads, 0, s, I->resid, dm + o_lrow, I->final_norm, I->lm_in,
-             m.d_model, m.rms_eps, (float*)nullptr, 0);
+             m.d_model, m.rms_eps);
     I->launches += 2;  // gathered RMSNorm + argmax
     I->launches += run_gemm(I->map_lm_in, I->lm_head, n_logit, I->logits, m.vocab, nullptr, tc::EPI_F32, I->sms, I->sk, s);
     launch_k(tc::argmax_rows<1024>, n_logit, 1024, 0, s, I->logits, m.vocab, I->ids_dev);
@@ -1495,7 +1449,7 @@ void destroy(tc_instance* I) {
   I->weight_owner.reset();
   I->pool.reset();
   f(I->resid); f(I->xnorm); f(I->qkv); f(I->attn_out); f(I->act); f(I->lm_in);
-  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->stream_scr); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
+  f(I->logits); f(I->ids_dev); f(I->sk.ws); f(I->sk.cnt); f(I->attn_ws_o); f(I->attn_ws_ml); f(I->attn_cnt); f(I->rope); f(I->meta_dev);
   if (I->ids_host) cudaFreeHost(I->ids_host);
   if (I->meta_host) cudaFreeHost(I->meta_host);
   for (cudaEvent_t e : {I->ev_start, I->ev_stop, I->mig_tail, I->ev_fork, I->ev_join})

@@ -4,7 +4,7 @@ benchmark"), on layer-reduced models (2 layers, every other dimension as benchma
 * config 2 (bench.py default): Llama-3-8B shapes, one step = a 512-token prefill chunk over a
   512-token paged prefix + 64 decodes at context 1024 (T = 576 rows), with the concurrent
   prefill | decode attention SM split active (attn_pf_sms > 0), plus the decode-only step of the
-  same 64 decodes (the weight-streaming split-K path);
+  same 64 decodes (T = 64: small token tiles, stream-K residual GEMMs);
 * config 5 (bench.py --model qwen2_5_14b --prefill 1024 --prefix 4096 --decode 32 --ctx 8192):
   Qwen2.5-14B shapes (QKV bias, GQA group 5), a 1024-token chunk over a 4096-token prefix + 32
   decodes at context 8192.

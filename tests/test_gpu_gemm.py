@@ -89,14 +89,18 @@ def test_gemm_f32_logits(cuda_ok, m, n, k):
 # the token tile TN = round_up(T / ceil(T / 256), 32) covers ragged T (1, 20, 100, 300, 1100 ...)
 @pytest.mark.parametrize("m,n,k", [(576, 6144, 4096), (1, 256, 128), (20, 512, 256), (100, 512, 1024),
                                    (300, 768, 512), (512, 1024, 4096), (1100, 1024, 4096), (3000, 512, 256),
-                                   (256, 256, 64), (129, 7168, 5120)])
+                                   (256, 256, 64), (129, 7168, 5120), (64, 6144, 4096), (64, 7168, 5120),
+                                   (1056, 7168, 5120)])
 def test_gemm_ws_bf16(cuda_ok, m, n, k):
+    # decode-only QKV shapes (64 x 6144 / 64 x 7168: fewer units than pairs) and config 5's
+    # (1056 x 7168, 5 token tiles); three back-to-back launches must give the same result
     g = torch.Generator(device="cuda").manual_seed(m * 13 + n + k)
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16, generator=g)
     b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16, generator=g)
-    out = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
-    _run(a, b, out, m, n, k, EPI_BF16, bn=1024)
-    _close(out, a.float() @ b.float().T, True)
+    for _ in range(3):
+        out = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
+        _run(a, b, out, m, n, k, EPI_BF16, bn=1024)
+        _close(out, a.float() @ b.float().T, True)
 
 
 # splits = 0: grouped stream-K (pair groups of one pair per token tile walk the weight-tile-major
@@ -116,15 +120,20 @@ def test_gemm_ws_residual(cuda_ok, m, n, k, splits):
     _close(resid, ref, False)
 
 
-@pytest.mark.parametrize("m,f,k", [(576, 14336, 4096), (97, 512, 256), (1100, 1024, 512)])
+# gate_up shapes of config 2 (576 x 28672: 336 units = 4 x 74 + 40), the decode-only step
+# (64 x 28672: 112 = 74 + 38) and config 5 (1056 x 27648, K = 5120: 540 units)
+@pytest.mark.parametrize("m,f,k", [(576, 14336, 4096), (97, 512, 256), (1100, 1024, 512), (64, 14336, 4096),
+                                   (1056, 13824, 5120)])
 def test_gemm_ws_swiglu(cuda_ok, m, f, k):
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     wg = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
     wu = torch.randn(f, k, device="cuda", dtype=torch.bfloat16) * 0.03
     phys = torch.stack([wg.view(f // 64, 64, k), wu.view(f // 64, 64, k)], dim=1).reshape(2 * f, k).contiguous()
-    out = torch.zeros(m, f, device="cuda", dtype=torch.bfloat16)
-    _run(a, phys, out, m, 2 * f, k, EPI_SWIGLU, bn=1024)
-    _close(out, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T), True)
+    ref = torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T)
+    for _ in range(2):
+        out = torch.zeros(m, f, device="cuda", dtype=torch.bfloat16)
+        _run(a, phys, out, m, 2 * f, k, EPI_SWIGLU, bn=1024)
+        _close(out, ref, True)
 
 
 def test_gemm_ws_bias_f32(cuda_ok):
