@@ -960,7 +960,7 @@ struct ProfScope {
 };
 
 // decode attention variant (A/B): TC_DEC_CFG="<consumer warps>:<producer warps>" (default 4:4;
-// tc::kDecVariants lists the compiled ones); TC_DEC_GRID caps the grid
+// tc::for_each_decode_variant_of lists the compiled ones); TC_DEC_GRID caps the grid
 std::pair<int, int> dec_cfg() {
   static const std::pair<int, int> c = [] {
     int nc = 4, np = 4;

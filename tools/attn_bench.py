@@ -4,7 +4,7 @@ attention phase (decode-only and mixed steps of BASELINE config 2) for each vari
 --variants ("ENV=a,ENV2=b ENV=c ..."), each in its own process (the library reads its A/B
 switches once per process), interleaved --rounds times so box drift hits every variant alike.
 
-  python tools/attn_bench.py --variants "TC_DEC_CFG=4:192 TC_DEC_CFG=6:192" --rounds 2
+  python tools/attn_bench.py --variants "TC_DEC_CFG=4:4 TC_DEC_CFG=6:4" --rounds 2
 """
 import argparse
 import json
@@ -58,7 +58,7 @@ def worker(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variants", default="TC_DEC_CFG=4:192")
+    ap.add_argument("--variants", default="TC_DEC_CFG=4:4")
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--model", default="llama3_8b")
     ap.add_argument("--layers", type=int, default=2)
