@@ -77,3 +77,11 @@ def test_config5_bench_step_qwen_shape():
     out, near = run_bench_step("qwen2_5_14b:L2", 5, P=1024, prefix=4096, D=32, ctx=8192, distinct=2, max_ctx=8256)
     assert out.attn_pf_sms > 0
     assert near <= 65 // 4
+
+
+def test_odd_step_shapes_llama():
+    """Off-bench sizes through the same path: a mixed step of T = 260 rows (2 token tiles of 160,
+    one ragged) and a decode-only step of T = 100 rows (one 128-token tile, 28 padded rows) --
+    the direct ws GEMM units with fused epilogues at token tiles the bench shapes do not hit."""
+    out, near = run_bench_step("llama3_8b:L2", 11, P=160, prefix=256, D=100, ctx=512, distinct=4, max_ctx=1024)
+    assert near <= 201 // 4
