@@ -411,7 +411,21 @@ int run_gemm_ws(ActMap& a, const WMat& w, int M, void* out, int ldo, const __nv_
     TC_REQUIRE(128 % rope->head_dim == 0, "gemm_ws: a 128-row half tile must cover whole heads");
     args.rope = *rope;
   }
-  const int grid = 2 * (int)std::min<long long>(pairs, args.units);
+  // Data-parallel units over the fewest pairs that keep the round count (decode-only gate_up:
+  // 112 units as 2 rounds of 56 pairs instead of 74 + 38; mixed gate_up: 5 rounds of 68): the
+  // weight stream of every round runs on equal SM counts. Measured: decode-only 5.145-5.149 vs
+  // 5.168-5.171 ms (three same-box rounds), config 2 61.4-61.8k vs 61.3k, config 5 neutral.
+  // TC_WS_BALANCE=0: min(pairs, units) (A/B).
+  static const bool balance = [] {
+    const char* e = std::getenv("TC_WS_BALANCE");
+    return !(e && e[0] == '0');
+  }();
+  long long used = std::min<long long>(pairs, args.units);
+  if (balance && !args.streamk && args.units > pairs) {
+    const long long rounds = (args.units + pairs - 1) / pairs;
+    used = (args.units + rounds - 1) / rounds;
+  }
+  const int grid = 2 * (int)used;
   // TC_WS_TRACE=1 (tools only): per-CTA %globaltimer timeline of this launch printed to stderr
   static const bool trace = std::getenv("TC_WS_TRACE") != nullptr;
   unsigned long long* trace_dev = nullptr;
